@@ -1,0 +1,152 @@
+/*
+ * ndgx.h -- C ABI of the B200-native NDG right-hand side + Runge-Kutta hot path.
+ *
+ * Drop-in boundary for the reference solver's stepping loop
+ * (/root/reference/proj; paths below are relative to it):
+ *
+ *   ndgx_create/ndgx_destroy  <- DGOperator ctor (src/solver.cpp:189-210) +
+ *                                RKIntegrator ctor (include/ndg/solver.hpp:41-44) +
+ *                                HaloSet::allocate (src/solver.cpp:159-164)
+ *   ndgx_upload/ndgx_download <- StateField hand-over (include/ndg/grid.hpp:50-56,
+ *                                AoS [cell_x][cell_y][cell_z][i][j][k][var])
+ *   ndgx_rhs                  <- serial_rhs (src/solver.cpp:442-456) /
+ *                                DGOperator::apply (src/solver.cpp:212-308)
+ *   ndgx_advance              <- advance (src/solver.cpp:372-440) with StepPlan
+ *                                (include/ndg/solver.hpp:168-171), StepStats (:153-158)
+ *   ndgx_decompose            <- decompose (src/partition.cpp:44-106)
+ *   ndgx_gauss_lobatto / ndgx_differentiation_matrix
+ *                             <- gauss_lobatto / differentiation_matrix
+ *                                (src/basis.cpp:32-76, 96-118), host setup inputs
+ *   ndgx_init_*               <- init_multisine / init_euler_subsonic
+ *                                (src/grid.cpp:135-188), host setup inputs
+ *
+ * Conventions (mirroring the reference): the caller owns every host buffer;
+ * a handle is used by one host thread at a time (like serial advance); all
+ * device memory belongs to the handle.  Every entry point returns an
+ * ndgx_status; a non-zero status fills the optional ndgx_error, whose code
+ * maps 1:1 onto include/ndg/errors.hpp:13-56.
+ *
+ * There is no CPU fallback: ndgx_create fails with NDGX_ERR_CUDA when no
+ * sm_100 device is present.
+ */
+#ifndef NDGX_H
+#define NDGX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NDGX_OK = 0,
+  NDGX_ERR_CONFIG = 1,        /* ndg::ConfigError        errors.hpp:13-16 */
+  NDGX_ERR_PHYSICS = 2,       /* ndg::PhysicsError       errors.hpp:19-22 */
+  NDGX_ERR_INSTABILITY = 3,   /* ndg::InstabilityError   errors.hpp:25-33 (step) */
+  NDGX_ERR_DECOMPOSITION = 4, /* ndg::DecompositionError errors.hpp:36-39 */
+  NDGX_ERR_TRANSPORT = 5,     /* ndg::TransportError     errors.hpp:42-45 (NCCL/P2P) */
+  NDGX_ERR_RUN = 6,           /* ndg::RunError           errors.hpp:48-56 (worker) */
+  NDGX_ERR_CUDA = 7           /* device / driver failure (no reference analogue) */
+} ndgx_status;
+
+typedef enum { NDGX_ADVECTION = 0, NDGX_EULER_ISOTHERMAL = 1 } ndgx_equation; /* models.hpp:26 */
+typedef enum { NDGX_RK3 = 0, NDGX_RK4 = 1, NDGX_RK6 = 2 } ndgx_rk;           /* solver.hpp:20 */
+
+/* Arithmetic mode.  EXACT reproduces the reference's IEEE-754 operation
+ * order with no contraction (bit-identical states); FAST lets the kernels
+ * contract into FMA (<= 1e-12 relative L2 vs the reference). */
+typedef enum { NDGX_ARITH_EXACT = 0, NDGX_ARITH_FAST = 1 } ndgx_arith;
+
+/* Mesh (grid.hpp:18-37) + EquationModel (models.hpp:43-73) +
+ * SolverConfig (solver.hpp:142-148).  Axes >= dim are ignored. */
+typedef struct {
+  int dim;              /* 1..3 */
+  int cells[3];         /* cells per axis (global) */
+  double length[3];     /* box edge lengths */
+  int order;            /* Gauss-Lobatto nodes per axis, 2..8 on the GPU path */
+  int equation;         /* ndgx_equation */
+  double velocity[3];   /* advection velocity */
+  double sound_speed;   /* isothermal Euler a > 0 */
+  int rk;               /* ndgx_rk */
+  double cfl;           /* (0, 1] */
+  double t_end;         /* > 0 */
+  /* optional basis, e.g. the caller's own gauss_lobatto/differentiation_matrix
+   * (NULL -> computed by ndgx_gauss_lobatto / ndgx_differentiation_matrix) */
+  const double* nodes;   /* [order] */
+  const double* weights; /* [order] */
+  const double* diff;    /* [order*order], diff[l*order+k] = h_k'(xi_l) (basis.hpp:22) */
+  int device;            /* CUDA device ordinal */
+  int arith;             /* ndgx_arith */
+} ndgx_problem;
+
+typedef struct { /* StepStats (solver.hpp:153-158); wall_seconds from CUDA events */
+  long steps;
+  double dt_min, dt_max, wall_seconds;
+} ndgx_stats;
+
+typedef struct {
+  int code;        /* ndgx_status */
+  long step;       /* InstabilityError::step() */
+  int stage;       /* RK stage of a PhysicsError in the operator, else -1 */
+  int worker;      /* RunError::worker(), else -1 */
+  int cell[3];     /* offending cell (global) for operator PhysicsErrors, else -1 */
+  char message[256];
+} ndgx_error;
+
+typedef struct ndgx_solver ndgx_solver;
+
+/* Lifecycle. */
+int ndgx_create(const ndgx_problem* problem, ndgx_solver** out, ndgx_error* err);
+void ndgx_destroy(ndgx_solver* s);
+
+/* State hand-over in the reference AoS layout (FieldShape::index order).
+ * host pointers may be pageable or pinned; the permutation to the device
+ * layout runs on the GPU. */
+int ndgx_upload(ndgx_solver* s, const double* u_aos, ndgx_error* err);
+int ndgx_download(ndgx_solver* s, double* u_aos, ndgx_error* err);
+
+/* serial_rhs of the current state into dudt_aos (host, AoS). */
+int ndgx_rhs(ndgx_solver* s, double* dudt_aos, ndgx_error* err);
+
+/* advance(config, state, StepPlan{fixed_steps, warmup}): fixed_steps < 0
+ * integrates to problem.t_end with the last step shortened.  The state stays
+ * on the device (download it afterwards). */
+int ndgx_advance(ndgx_solver* s, long fixed_steps, int warmup, ndgx_stats* stats,
+                 ndgx_error* err);
+
+/* Sizes. */
+int64_t ndgx_dof(const ndgx_solver* s);      /* cells * order^dim * n_var (grid.cpp:72-74) */
+size_t ndgx_state_size(const ndgx_solver* s); /* doubles in one state (== dof) */
+int ndgx_stages(const ndgx_solver* s);
+
+/* Device-resident stepping for benchmarks: launch `steps` fixed CFL steps
+ * on the handle's stream without host synchronisation or error polling
+ * (call ndgx_sync to collect errors).  ndgx_stream returns the cudaStream_t. */
+int ndgx_launch_steps(ndgx_solver* s, long steps, ndgx_error* err);
+int ndgx_sync(ndgx_solver* s, ndgx_stats* stats, ndgx_error* err);
+void* ndgx_stream(ndgx_solver* s);
+/* Per-kernel timing of one un-graphed step (CUDA events on the launching
+ * stream): ms[i] for stage kernel i, plus the step-control kernel at ms[stages]. */
+int ndgx_profile_step(ndgx_solver* s, float* ms, int n, ndgx_error* err);
+
+/* Host setup inputs (same arithmetic as the reference). */
+int ndgx_gauss_lobatto(int order, double* nodes, double* weights);
+int ndgx_differentiation_matrix(int order, const double* nodes, double* diff);
+int ndgx_init_multisine(const ndgx_problem* p, const double* amplitudes, int n_modes,
+                        double* u_aos);
+void ndgx_multisine_amplitudes(int n_modes, uint64_t seed, double* out);
+int ndgx_init_euler_subsonic(const ndgx_problem* p, double* u_aos);
+
+/* Block decomposition (partition.cpp:44-106): grid[3]; lo/hi [workers][3];
+ * nbr [workers][3][2] (low, high). */
+int ndgx_decompose(int dim, const int cells[3], int workers, int grid[3], int* lo, int* hi,
+                   int* nbr, ndgx_error* err);
+
+/* Library identification: "ndgx <version> sm_100a". */
+const char* ndgx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NDGX_H */

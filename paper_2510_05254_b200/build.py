@@ -1,0 +1,75 @@
+"""Build the sm_100a extension in-tree: paper_2510_05254_b200/libndgx.so.
+
+    python -m paper_2510_05254_b200.build [--force]
+
+nvcc cross-compiles for sm_100a without a GPU.  Each translation unit is
+compiled in parallel; the result is a self-contained shared library (static
+cudart) exporting the C ABI declared in include/ndgx.h.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+BUILD = os.path.join(PKG, "_build")
+LIB = os.path.join(PKG, "libndgx.so")
+
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
+         "-I", INCLUDE, "-I", CSRC]
+
+SOURCES = ["ndgx_inst_d1.cu", "ndgx_inst_d2.cu", "ndgx_inst_d3.cu", "ndgx_solver.cu",
+           "ndgx_setup.cpp"]
+HEADERS = ["ndgx_device.cuh", "ndgx_kernels.h", "ndgx_setup.h"]
+
+
+def _stale(obj: str, src: str) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    deps = [src, os.path.join(INCLUDE, "ndgx.h")] + [os.path.join(CSRC, h) for h in HEADERS]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _compile(src: str) -> str:
+    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+    path = os.path.join(CSRC, src)
+    if _stale(obj, path):
+        cmd = [NVCC] + ARCH + FLAGS + ["-c", path, "-o", obj]
+        if src.endswith(".cpp"):
+            cxx = os.environ.get("CXX", shutil.which("g++") or "g++")
+            cmd = [cxx, "-O2", "-fPIC", "-ffp-contract=off", "-std=c++17", "-I", INCLUDE, "-I", CSRC,
+                   "-c", path, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+    return obj
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    if force:
+        for f in os.listdir(BUILD):
+            os.remove(os.path.join(BUILD, f))
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(_compile, SOURCES))
+    if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stderr}")
+    if verbose:
+        print("built", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

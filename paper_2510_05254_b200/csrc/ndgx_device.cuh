@@ -1,0 +1,661 @@
+// ndgx_device.cuh -- sm_100a kernels of the fused NDG RHS + RK stage update.
+//
+// Reference semantics (paths relative to /root/reference/proj):
+//   volume term      src/solver.cpp:229-262   (per axis, K-row dot, out += acc)
+//   face term        src/solver.cpp:264-306   (LF flux, -/+ lift)
+//   physical flux    src/models.cpp:42-57, wavespeed :59-75, LF :77-88
+//   RK stage update  include/ndg/solver.hpp:49-76
+//   CFL alpha scan   src/solver.cpp:310-334, dt_from_alpha :336-341
+//   finite check     src/solver.cpp:361-368
+//
+// Device layout (SoA, node-fastest, element-blocked):
+//   a[((e * NV + v) * NPE) + n],  e = cx + C0*(cy + C1*cz),  n = i + N*(j + N*k)
+// so one element's variable is NPE contiguous doubles (512 B at 2D N=8 and
+// at 3D N=4) and each x-line is N contiguous doubles.
+//
+// One CTA owns a tile of TE consecutive x-cells.  Phase X: one thread per
+// x-line loads the stage input U_s = u + sum_j a_sj K_j (on the fly, in the
+// reference's term order), evaluates every axis' flux at its nodes, applies
+// the x volume term from registers and the x faces (in-tile neighbours via
+// shared memory, others from global/L2).  Phase Y (and Z) re-partition the
+// tile into y-lines (z-lines) through shared memory and add their volume and
+// face terms in the reference's per-node order vol_x, face_x, vol_y, face_y,
+// vol_z, face_z.  The owner of the last phase runs the RK epilogue:
+// K_s = dt * dudt (stored), or at the last stage u_new = S + b_s K_s with
+// S = u + sum_{j<s} b_j K_j formed in phase X -- plus the finite check and
+// the next step's wavespeed max-reduction (warp shuffle -> block -> atomicMax).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ndgx {
+
+constexpr int kMaxOrder = 8;
+constexpr int kMaxTerms = 6;
+constexpr unsigned long long kNoError = ~0ull;
+
+// Error-key phases, ordered like the reference's execution within a step.
+enum : int {
+  kPhaseScan = 0,        // max_wavespeed_bound PhysicsError (solver.cpp:325-328)
+  kPhaseZeroSpeed = 1,   // fixed-step ConfigError (solver.cpp:411-413)
+  kPhaseStage0 = 2,      // 2 + stage: operator PhysicsError (solver.cpp:258-261)
+  kPhaseInstability = 9  // check_finite InstabilityError (solver.cpp:361-368)
+};
+
+__host__ __device__ inline unsigned long long error_key(long long step, int phase,
+                                                        long long cell, int node) {
+  return ((unsigned long long)(step & 0xFFFFF) << 44) | ((unsigned long long)(phase & 0xF) << 40) |
+         ((unsigned long long)(cell & 0xFFFFFFF) << 12) | (unsigned long long)(node & 0xFFF);
+}
+
+// Device-resident step control (advance, solver.cpp:405-436).
+struct Control {
+  unsigned long long alpha_bits;  // running max wavespeed of the current state (>= 0)
+  unsigned long long err_key;     // first error in reference execution order
+  double dt;
+  double t;
+  double dt_min;
+  double dt_max;
+  long long steps;                // steps begun
+  int skip;                       // current step inactive (done / error)
+  int done;                       // t_end reached
+};
+
+struct StepParams {
+  Control* ctl;
+  long long fixed_steps;  // < 0: t_end mode
+  double t_end;
+  double cflh;            // cfl * min_d dx_d  (dt_from_alpha numerator)
+  double two_n_minus_1;   // (2N - 1)
+  double const_alpha;     // advection: max_d |a_d|; < 0 for Euler (scanned)
+  int warmup;             // warm-up step: non-finite dt -> t_end, no stats
+};
+
+struct StageArgs {
+  const double* u;                 // u^n
+  const double* ka[kMaxTerms];     // stage-input terms (ascending j, a_sj != 0)
+  double ca[kMaxTerms];
+  const double* kb[kMaxTerms];     // last stage: S = u + sum b_j K_j (ascending j, b_j != 0)
+  double cb[kMaxTerms];
+  double* out;                     // K_s, or u_new at the last stage
+  Control* ctl;
+  double b_last;
+  int na, nb;
+  int is_last;
+  int rhs_only;                    // serial_rhs: dt := 1, no step control
+  int phase;                       // kPhaseStage0 + stage
+  int scan_alpha;                  // last stage of an Euler run: reduce next alpha
+  int cells[3];                    // local block
+  int gcells[3];                   // global mesh (error cell naming)
+  int goff[3];                     // block offset in the global mesh
+  double sound_speed;
+  double vel[3];
+  double lift[3];
+  double K[3][kMaxOrder * kMaxOrder];  // K_d[k*N + l] (solver.cpp:203-207)
+};
+
+// ------------------------------------------------------------- arithmetic
+template <bool EXACT>
+struct Ar;
+
+template <>
+struct Ar<true> {  // reference IEEE order, no contraction
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double mac(double acc, double a, double b) {
+    return __dadd_rn(acc, __dmul_rn(a, b));
+  }
+};
+
+template <>
+struct Ar<false> {  // contracted
+  static __device__ __forceinline__ double add(double a, double b) { return a + b; }
+  static __device__ __forceinline__ double sub(double a, double b) { return a - b; }
+  static __device__ __forceinline__ double mul(double a, double b) { return a * b; }
+  static __device__ __forceinline__ double div(double a, double b) { return a / b; }
+  static __device__ __forceinline__ double mac(double acc, double a, double b) {
+    return fma(a, b, acc);
+  }
+};
+
+__device__ __forceinline__ double dmax(double a, double b) { return (a < b) ? b : a; }
+
+template <int DIM, int N, int KIND>
+struct Geo {
+  static constexpr int NV = (KIND == 0) ? 1 : DIM + 1;
+  static constexpr int L = (DIM == 1) ? 1 : (DIM == 2 ? N : N * N);  // lines per element
+  static constexpr int NPE = L * N;                                   // nodes per element
+  static constexpr int NPEP = L * (N + 1);  // padded shared-memory element stride
+  static constexpr int TE = (128 / L) < 1 ? 1 : (128 / L);            // elements per tile
+  static constexpr int THREADS = TE * L;
+  static constexpr int ARR = TE * NV * NPEP;  // doubles in one shared field tile
+  static constexpr int TRC = TE * 2 * NV * L; // doubles in one axis' trace buffer
+  // shared memory carve-up (doubles): F[1..DIM-1], P, traces[DIM], red[32], S (last stage)
+  static constexpr int OFF_F = 0;
+  static constexpr int OFF_P = OFF_F + (DIM - 1) * ARR;
+  static constexpr int OFF_T = OFF_P + (DIM > 1 ? ARR : 0);
+  static constexpr int OFF_R = OFF_T + DIM * TRC;
+  static constexpr int OFF_S = OFF_R + 32;
+  static constexpr int SMEM_BASE = OFF_S * 8;
+  static constexpr int SMEM_LAST = (OFF_S + (DIM > 1 ? ARR : 0)) * 8;
+
+  // node index of position k along `axis` for transverse line index tr
+  static __device__ __forceinline__ int node(int axis, int tr, int k) {
+    if (axis == 0) return k + N * tr;
+    if (axis == 1) return (tr % N) + N * (k + N * (tr / N));
+    return tr + N * N * k;
+  }
+  // padded shared-memory slot of node n (x-lines padded to N+1: conflict-free
+  // for both x-line owners and y/z-line owners)
+  static __device__ __forceinline__ int sn(int n) { return n + n / N; }
+  // AoS node order inside a cell (grid.hpp:50-56): i slowest
+  static __device__ __forceinline__ int aos_node(int n) {
+    const int i = n % N;
+    if (DIM == 1) return i;
+    const int j = (n / N) % N;
+    if (DIM == 2) return i * N + j;
+    return (i * N + j) * N + n / (N * N);
+  }
+};
+
+// F_axis(u) and the one-sided wavespeed bound (models.cpp:42-70).
+template <int DIM, int KIND, bool EXACT>
+__device__ __forceinline__ void flux(const StageArgs& p, const double* u, int axis, double* f,
+                                     double& speed) {
+  using A = Ar<EXACT>;
+  if (KIND == 0) {
+    f[0] = A::mul(p.vel[axis], u[0]);
+    speed = fabs(p.vel[axis]);
+  } else {
+    constexpr int NV = DIM + 1;
+    const double rho = u[0];
+    const double ua = A::div(u[1 + axis], rho);
+    f[0] = u[1 + axis];
+#pragma unroll
+    for (int i = 1; i < NV; ++i) f[i] = A::mul(ua, u[i]);
+    f[1 + axis] = A::add(f[1 + axis], A::mul(A::mul(rho, p.sound_speed), p.sound_speed));
+    speed = A::add(fabs(ua), p.sound_speed);
+  }
+}
+
+// Lax-Friedrichs flux from both one-sided fluxes and speeds (models.cpp:77-88).
+template <int NV, bool EXACT>
+__device__ __forceinline__ void lax_friedrichs(const double* um, const double* up,
+                                               const double* fm, const double* fp, double sm,
+                                               double sp, double* fhat) {
+  using A = Ar<EXACT>;
+  const double alpha = dmax(sm, sp);
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+    fhat[v] = A::mul(0.5, A::sub(A::add(fm[v], fp[v]), A::mul(alpha, A::sub(up[v], um[v]))));
+}
+
+// Stage input at one global index: stage_ = u; stage_ += a_sj k_j (solver.hpp:55-62).
+template <bool EXACT>
+__device__ __forceinline__ double stage_input(const StageArgs& p, size_t idx) {
+  using A = Ar<EXACT>;
+  double s = __ldg(p.u + idx);
+  for (int t = 0; t < p.na; ++t) s = A::mac(s, p.ca[t], __ldg(p.ka[t] + idx));
+  return s;
+}
+
+__device__ __forceinline__ void record_error(Control* ctl, unsigned long long key) {
+  if (key < *(volatile unsigned long long*)&ctl->err_key) atomicMin(&ctl->err_key, key);
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ============================================================ stage kernel
+template <int DIM, int N, int KIND, bool EXACT>
+__global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS)
+stage_kernel(const __grid_constant__ StageArgs p) {
+  using G = Geo<DIM, N, KIND>;
+  using A = Ar<EXACT>;
+  constexpr int NV = G::NV, L = G::L, NPE = G::NPE, NPEP = G::NPEP, TE = G::TE;
+  extern __shared__ double smem[];
+
+  Control* ctl = p.ctl;
+  // inactive step, or an earlier stage already failed: keep the inputs of the
+  // failing stage intact for the host's error report
+  if (!p.rhs_only && (*(volatile int*)&ctl->skip ||
+                      *(volatile unsigned long long*)&ctl->err_key != kNoError))
+    return;
+
+  const int C0 = p.cells[0], C1 = p.cells[1], C2 = p.cells[2];
+  (void)C2;
+  const int ntx = (C0 + TE - 1) / TE;
+  const int bid = blockIdx.x;
+  const int tx = bid % ntx;
+  const int rest = bid / ntx;
+  const int cy = rest % C1;
+  const int cz = rest / C1;
+  const int x0 = tx * TE;
+  const int nvalid = min(TE, C0 - x0);
+
+  const int tid = threadIdx.x;
+  const int el = tid / L;
+  const int tr = tid % L;  // transverse line index (same count for every axis)
+  const bool valid = el < nvalid;
+  const int cx = x0 + el;
+  const size_t e = (size_t)cx + (size_t)C0 * ((size_t)cy + (size_t)C1 * cz);
+  const size_t ebase = e * NV * NPE;
+
+  const double dt = p.rhs_only ? 1.0 : ctl->dt;
+  const long long step = p.rhs_only ? 0 : ctl->steps;
+
+  double* sF = smem + G::OFF_F;  // [DIM-1][TE][NV][NPEP]
+  double* sP = smem + G::OFF_P;  // [TE][NV][NPEP]
+  double* sT = smem + G::OFF_T;  // [DIM][TE][2][NV][L]
+  double* sR = smem + G::OFF_R;  // [32]
+  double* sS = smem + G::OFF_S;  // [TE][NV][NPEP] (last stage, DIM > 1)
+
+  auto trc = [&](int axis, int elx, int side, int v, int t) -> double& {
+    return sT[(((axis * TE + elx) * 2 + side) * NV + v) * L + t];
+  };
+  auto fld = [&](double* base, int elx, int v, int n) -> double& {
+    return base[(elx * NV + v) * NPEP + G::sn(n)];
+  };
+  auto aos_cell = [&](int x, int y, int z) -> long long {  // global AoS cell index
+    const long long gx = x + p.goff[0], gy = y + p.goff[1], gz = z + p.goff[2];
+    return (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz;
+  };
+
+  // ---------------------------------------------------------------- phase X
+  double D[NV][N];
+  double S[NV][N];
+  double f_lo[NV], f_hi[NV], u_lo[NV], u_hi[NV];
+  double s_lo = 0.0, s_hi = 0.0;
+  (void)S;
+  if (valid) {
+    double U[NV][N];
+    const size_t lb = ebase + (size_t)tr * N;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int i = 0; i < N; ++i) U[v][i] = __ldg(p.u + lb + (size_t)v * NPE + i);
+    if (p.is_last) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int i = 0; i < N; ++i) S[v][i] = U[v][i];
+    }
+    for (int t = 0; t < p.na; ++t) {
+      const double* kt = p.ka[t] + lb;
+      const double c = p.ca[t];
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int i = 0; i < N; ++i) U[v][i] = A::mac(U[v][i], c, __ldg(kt + (size_t)v * NPE + i));
+    }
+    if (p.is_last) {
+      for (int t = 0; t < p.nb; ++t) {
+        const double* kt = p.kb[t] + lb;
+        const double c = p.cb[t];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int i = 0; i < N; ++i) S[v][i] = A::mac(S[v][i], c, __ldg(kt + (size_t)v * NPE + i));
+      }
+      if (DIM > 1) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int i = 0; i < N; ++i) fld(sS, el, v, i + N * tr) = S[v][i];
+      }
+    }
+
+    // fluxes at every node of the line, every axis
+    double FX[NV][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double un[NV], f[NV], sp;
+      if (KIND == 1 && !(U[0][i] > 0.0)) {
+        // first bad node of the reference's x-volume traversal: (cell, (j,k), i)
+        const int j = (DIM > 1) ? tr % N : 0, k = (DIM > 2) ? tr / N : 0;
+        const int nkey = (DIM == 1) ? i : (DIM == 2 ? j * N + i : (j * N + k) * N + i);
+        record_error(ctl, error_key(step, p.phase, aos_cell(cx, cy, cz), nkey));
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) un[v] = U[v][i];
+      flux<DIM, KIND, EXACT>(p, un, 0, f, sp);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) FX[v][i] = f[v];
+      if (i == 0) s_lo = sp;
+      if (i == N - 1) s_hi = sp;
+#pragma unroll
+      for (int d = 1; d < DIM; ++d) {
+        flux<DIM, KIND, EXACT>(p, un, d, f, sp);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) fld(sF + (d - 1) * G::ARR, el, v, i + N * tr) = f[v];
+      }
+    }
+    // volume x: out(=0) += sum_l K[k][l] F_l   (solver.cpp:246-256)
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) acc = A::mac(acc, p.K[0][k * N + l], FX[v][l]);
+        D[v][k] = A::add(0.0, acc);
+      }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      f_lo[v] = FX[v][0];
+      f_hi[v] = FX[v][N - 1];
+      u_lo[v] = U[v][0];
+      u_hi[v] = U[v][N - 1];
+      trc(0, el, 0, v, tr) = U[v][0];  // own x traces for in-tile neighbours
+      trc(0, el, 1, v, tr) = U[v][N - 1];
+    }
+    if (DIM > 1) {  // own y/z face traces for the later phases
+      const int j = tr % N, k = tr / N;
+      if (j == 0 || j == N - 1) {
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) trc(1, el, j == 0 ? 0 : 1, v, i + N * k) = U[v][i];
+      }
+      if (DIM > 2 && (k == 0 || k == N - 1)) {
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) trc(2, el, k == 0 ? 0 : 1, v, i + N * j) = U[v][i];
+      }
+    }
+  }
+  __syncthreads();
+
+  // x faces (solver.cpp:268-306): face at i=0 (we are its + side) and at
+  // i=N-1 (we are its - side).  The minus state is always the lower cell.
+  if (valid) {
+    double nb_lo[NV], nb_hi[NV];
+    const int xl = (cx == 0) ? C0 - 1 : cx - 1;
+    const int xr = (cx == C0 - 1) ? 0 : cx + 1;
+    if (xl >= x0 && xl < x0 + nvalid) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) nb_lo[v] = trc(0, xl - x0, 1, v, tr);
+    } else {
+      const size_t nbase = ((size_t)xl + (size_t)C0 * ((size_t)cy + (size_t)C1 * cz)) * NV * NPE;
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        nb_lo[v] = stage_input<EXACT>(p, nbase + (size_t)v * NPE + (N - 1) + (size_t)N * tr);
+    }
+    if (xr >= x0 && xr < x0 + nvalid) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) nb_hi[v] = trc(0, xr - x0, 0, v, tr);
+    } else {
+      const size_t nbase = ((size_t)xr + (size_t)C0 * ((size_t)cy + (size_t)C1 * cz)) * NV * NPE;
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        nb_hi[v] = stage_input<EXACT>(p, nbase + (size_t)v * NPE + (size_t)N * tr);
+    }
+    double fn[NV], sn, fhat[NV];
+    const double lift = p.lift[0];
+    flux<DIM, KIND, EXACT>(p, nb_lo, 0, fn, sn);
+    lax_friedrichs<NV, EXACT>(nb_lo, u_lo, fn, f_lo, sn, s_lo, fhat);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) D[v][0] = A::add(D[v][0], A::mul(lift, fhat[v]));
+    flux<DIM, KIND, EXACT>(p, nb_hi, 0, fn, sn);
+    lax_friedrichs<NV, EXACT>(u_hi, nb_hi, f_hi, fn, s_hi, sn, fhat);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) D[v][N - 1] = A::sub(D[v][N - 1], A::mul(lift, fhat[v]));
+    if (DIM > 1) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int i = 0; i < N; ++i) fld(sP, el, v, i + N * tr) = D[v][i];
+    }
+  }
+
+  // -------------------------------------------------------- phases Y and Z
+#pragma unroll
+  for (int axis = 1; axis < DIM; ++axis) {
+    __syncthreads();
+    if (valid) {
+      double F[NV][N];
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int k = 0; k < N; ++k) F[v][k] = fld(sF + (axis - 1) * G::ARR, el, v, G::node(axis, tr, k));
+      // volume: partial + sum_l K[k][l] F_l
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < N; ++l) acc = A::mac(acc, p.K[axis][k * N + l], F[v][l]);
+          D[v][k] = A::add(fld(sP, el, v, G::node(axis, tr, k)), acc);
+        }
+      // faces along this axis
+      double a_lo[NV], a_hi[NV], nb_lo[NV], nb_hi[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        a_lo[v] = trc(axis, el, 0, v, tr);
+        a_hi[v] = trc(axis, el, 1, v, tr);
+      }
+      const int cn = p.cells[axis];
+      const int ca = (axis == 1) ? cy : cz;
+      const int lo_c = (ca == 0) ? cn - 1 : ca - 1;
+      const int hi_c = (ca == cn - 1) ? 0 : ca + 1;
+      if (cn == 1) {  // single cell along this axis: periodic self-neighbour
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          nb_lo[v] = a_hi[v];
+          nb_hi[v] = a_lo[v];
+        }
+      } else {
+        const int ly = (axis == 1) ? lo_c : cy, lz = (axis == 2) ? lo_c : cz;
+        const int hy = (axis == 1) ? hi_c : cy, hz = (axis == 2) ? hi_c : cz;
+        const size_t lbase = ((size_t)cx + (size_t)C0 * ((size_t)ly + (size_t)C1 * lz)) * NV * NPE;
+        const size_t hbase = ((size_t)cx + (size_t)C0 * ((size_t)hy + (size_t)C1 * hz)) * NV * NPE;
+        const int n_lo = G::node(axis, tr, N - 1), n_hi = G::node(axis, tr, 0);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          nb_lo[v] = stage_input<EXACT>(p, lbase + (size_t)v * NPE + n_lo);
+          nb_hi[v] = stage_input<EXACT>(p, hbase + (size_t)v * NPE + n_hi);
+        }
+      }
+      double fo[NV], so, fn[NV], sn, fhat[NV];
+      const double lift = p.lift[axis];
+      flux<DIM, KIND, EXACT>(p, nb_lo, axis, fn, sn);
+      flux<DIM, KIND, EXACT>(p, a_lo, axis, fo, so);
+      lax_friedrichs<NV, EXACT>(nb_lo, a_lo, fn, fo, sn, so, fhat);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) D[v][0] = A::add(D[v][0], A::mul(lift, fhat[v]));
+      flux<DIM, KIND, EXACT>(p, nb_hi, axis, fn, sn);
+      flux<DIM, KIND, EXACT>(p, a_hi, axis, fo, so);
+      lax_friedrichs<NV, EXACT>(a_hi, nb_hi, fo, fn, so, sn, fhat);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) D[v][N - 1] = A::sub(D[v][N - 1], A::mul(lift, fhat[v]));
+      if (axis < DIM - 1) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int k = 0; k < N; ++k) fld(sP, el, v, G::node(axis, tr, k)) = D[v][k];
+      }
+    }
+  }
+
+  // ------------------------------------------------------------ epilogue
+  constexpr int FA = DIM - 1;  // axis of the final owner
+  double alpha = 0.0;
+  if (valid) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int n = G::node(FA, tr, k);
+      double kv[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) kv[v] = A::mul(D[v][k], dt);  // k_i *= dt (solver.hpp:66-67)
+      if (!p.is_last) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) p.out[ebase + (size_t)v * NPE + n] = kv[v];
+      } else {
+        double un[NV];
+        bool finite = true;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double s = (DIM > 1) ? fld(sS, el, v, n) : S[v][k];
+          un[v] = A::mac(s, p.b_last, kv[v]);  // u += b_i k_i (solver.hpp:69-75)
+          p.out[ebase + (size_t)v * NPE + n] = un[v];
+          finite = finite && isfinite(un[v]);
+        }
+        if (!finite) record_error(ctl, error_key(step, kPhaseInstability, 0, 0));
+        if (KIND == 1 && p.scan_alpha) {
+          // the next step's max_wavespeed_bound (solver.cpp:323-332), fused
+          if (!(un[0] > 0.0)) {
+            record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(cx, cy, cz), G::aos_node(n)));
+          } else {
+            double m = 0.0;
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) m = dmax(m, fabs(un[1 + d]));
+            alpha = dmax(alpha, A::add(A::div(m, un[0]), p.sound_speed));
+          }
+        }
+      }
+    }
+  }
+  if (KIND == 1 && p.is_last && p.scan_alpha) {
+    alpha = warp_max(alpha);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) sR[warp] = alpha;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0;
+      for (int w = 0; w < (G::THREADS + 31) / 32; ++w) a = dmax(a, sR[w]);
+      atomicMax(&ctl->alpha_bits, (unsigned long long)__double_as_longlong(a));
+    }
+  }
+}
+
+// ============================================================ alpha scan
+// max_wavespeed_bound over a device-layout state (solver.cpp:310-334).
+template <int DIM>
+__global__ void alpha_scan_kernel(const double* __restrict__ u, int c0, int c1, int c2, int order,
+                                  double a, Control* ctl, long long step_for_error) {
+  constexpr int NV = DIM + 1;
+  const int npe = DIM == 2 ? order * order : order * order * order;
+  const long long n_elem = (long long)c0 * c1 * c2;
+  const long long total = n_elem * npe;
+  double alpha = 0.0;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long e = q / npe;
+    const int n = (int)(q - e * npe);
+    const double* base = u + e * NV * npe + n;
+    const double rho = base[0];
+    if (!(rho > 0.0)) {
+      const int cx = (int)(e % c0), cy = (int)((e / c0) % c1), cz = (int)(e / ((long long)c0 * c1));
+      const int i = n % order, j = (n / order) % order, k = n / (order * order);
+      const int an = DIM == 2 ? i * order + j : (i * order + j) * order + k;
+      record_error(ctl, error_key(step_for_error, kPhaseScan,
+                                  ((long long)cx * c1 + cy) * c2 + cz, an));
+      continue;
+    }
+    double m = 0.0;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) m = dmax(m, fabs(base[(size_t)(1 + d) * npe]));
+    alpha = dmax(alpha, __dadd_rn(__ddiv_rn(m, rho), a));
+  }
+  alpha = warp_max(alpha);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = alpha;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) m = dmax(m, red[w]);
+    atomicMax(&ctl->alpha_bits, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+// ============================================================ step control
+// One thread: dt_from_alpha (solver.cpp:336-341) + the fixed-step / t_end
+// loop bookkeeping of advance (solver.cpp:407-436), without host round trips.
+static __global__ void step_begin_kernel(StepParams sp) {
+  Control* c = sp.ctl;
+  if (c->err_key != kNoError || c->done) {
+    c->skip = 1;
+    return;
+  }
+  const bool fixed = sp.fixed_steps >= 0;
+  if ((fixed && c->steps >= sp.fixed_steps) || (!fixed && !(c->t < sp.t_end))) {
+    c->done = 1;
+    c->skip = 1;
+    return;
+  }
+  const double alpha = sp.const_alpha >= 0.0 ? sp.const_alpha : __longlong_as_double((long long)c->alpha_bits);
+  const double stable = (alpha <= 0.0) ? __longlong_as_double(0x7ff0000000000000LL)
+                                       : __ddiv_rn(sp.cflh, __dmul_rn(alpha, sp.two_n_minus_1));
+  double dt;
+  if (sp.warmup) {
+    dt = isfinite(stable) ? stable : sp.t_end;
+    c->steps = 1;
+    c->done = 1;  // a warm-up is exactly one step
+  } else {
+    const long long step = ++c->steps;
+    if (fixed) {
+      if (!isfinite(stable)) {
+        atomicMin(&c->err_key, error_key(step, kPhaseZeroSpeed, 0, 0));
+        c->skip = 1;
+        return;
+      }
+      dt = stable;
+    } else {
+      const double remaining = __dsub_rn(sp.t_end, c->t);
+      const bool last = remaining <= stable;
+      dt = last ? remaining : stable;
+      if (last) c->done = 1;
+      else c->t = __dadd_rn(c->t, dt);
+    }
+    c->dt_min = (dt < c->dt_min) ? dt : c->dt_min;
+    c->dt_max = (c->dt_max < dt) ? dt : c->dt_max;
+  }
+  c->dt = dt;
+  c->skip = 0;
+  c->alpha_bits = 0ull;  // this step's last-stage epilogue accumulates the next alpha
+}
+
+// ===================================================== layout permutation
+// AoS (FieldShape::index, grid.hpp:50-56) <-> device SoA element-blocked.
+template <bool TO_DEVICE>
+__global__ void permute_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                               int dim, int c0, int c1, int c2, int order, int nv,
+                               long long total) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    // q enumerates the device layout: ((e*nv + v)*npe + n)
+    int npe = order;
+    if (dim > 1) npe *= order;
+    if (dim > 2) npe *= order;
+    const long long n = q % npe;
+    const long long ev = q / npe;
+    const int v = (int)(ev % nv);
+    const long long e = ev / nv;
+    const int cx = (int)(e % c0);
+    const long long r = e / c0;
+    const int cy = (int)(r % c1);
+    const int cz = (int)(r / c1);
+    const int i = (int)(n % order);
+    const int j = dim > 1 ? (int)((n / order) % order) : 0;
+    const int k = dim > 2 ? (int)(n / ((long long)order * order)) : 0;
+    long long idx = cx;
+    if (dim > 1) idx = idx * c1 + cy;
+    if (dim > 2) idx = idx * c2 + cz;
+    idx = idx * order + i;
+    if (dim > 1) idx = idx * order + j;
+    if (dim > 2) idx = idx * order + k;
+    idx = idx * nv + v;
+    if (TO_DEVICE) dst[q] = src[idx];
+    else dst[idx] = src[q];
+  }
+}
+
+}  // namespace ndgx

@@ -1,0 +1,670 @@
+// ndgx_solver.cu -- the C ABI (include/ndgx.h): device state, step loop,
+// CUDA-graph capture, error mapping onto the reference's exception taxonomy.
+//
+// Reference (paths relative to /root/reference/proj):
+//   advance            src/solver.cpp:372-440     -> ndgx_advance
+//   serial_rhs         src/solver.cpp:442-456     -> ndgx_rhs
+//   RKIntegrator       include/ndg/solver.hpp:39-82 (buffers :41-44)
+//   errors             include/ndg/errors.hpp:13-56
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "ndgx.h"
+#include "ndgx_kernels.h"
+#include "ndgx_setup.h"
+
+using ndgx::Control;
+using ndgx::StageArgs;
+using ndgx::StepParams;
+
+namespace {
+
+void set_error(ndgx_error* e, int code, const std::string& msg, long step = 0, int stage = -1,
+               const int* cell = nullptr) {
+  if (!e) return;
+  std::memset(e, 0, sizeof(*e));
+  e->code = code;
+  e->step = step;
+  e->stage = stage;
+  e->worker = -1;
+  for (int a = 0; a < 3; ++a) e->cell[a] = cell ? cell[a] : -1;
+  std::snprintf(e->message, sizeof(e->message), "%s", msg.c_str());
+}
+
+void clear_error(ndgx_error* e) {
+  if (!e) return;
+  std::memset(e, 0, sizeof(*e));
+  e->stage = -1;
+  e->worker = -1;
+  e->cell[0] = e->cell[1] = e->cell[2] = -1;
+}
+
+struct CudaFailure {
+  cudaError_t rc;
+  const char* what;
+};
+
+inline void ck(cudaError_t rc, const char* what) {
+  if (rc != cudaSuccess) throw CudaFailure{rc, what};
+}
+
+std::string fmt_double(double v) {  // std::to_string(double) == "%f"
+  char b[64];
+  std::snprintf(b, sizeof(b), "%f", v);
+  return b;
+}
+
+}  // namespace
+
+struct ndgx_solver {
+  ndgx_problem p{};
+  int dim = 0, N = 0, nv = 0, kind = 0, stages = 0, npe = 0;
+  int cells[3] = {1, 1, 1};
+  size_t n = 0;
+  int64_t dof = 0;
+  bool exact = true;
+  double K[3][64]{}, lift[3]{}, a[7][7]{}, b[7]{};
+  double cflh = 0.0, two_n_minus_1 = 0.0, const_alpha = -1.0;
+  ndgx::StageKernel kern;
+  cudaStream_t stream = nullptr;
+  std::vector<double*> buf;
+  int dead = -1;      // K slot overwritten by u_new at the last stage (-1: none)
+  int parity = 0;     // u lives in buf[parity]
+  Control* ctl = nullptr;
+  Control* ctl_warm = nullptr;
+  Control* h_ctl = nullptr;  // pinned mirror
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  long long graph_fixed = -2;
+  double graph_tend = -1.0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  long long pending_fixed = -1;  // ndgx_launch_steps bookkeeping
+  int pending_start_parity = 0;
+
+  // ------------------------------------------------------------ buffers
+  double* u_buf(int par) const { return buf[par]; }
+  double* out_buf(int par) const { return buf[1 - par]; }
+  double* k_buf(int j, int par) const {
+    if (j == dead) return buf[1 - par];
+    int rank = j;
+    if (dead >= 0 && j > dead) --rank;
+    return buf[2 + rank];
+  }
+  double* staging(int par) const {
+    double* r = k_buf(0, par);
+    return r != buf[1 - par] ? buf[1 - par] : buf[2];
+  }
+
+  StageArgs stage_args(int i, int par, Control* c, bool rhs_only) const {
+    StageArgs s;
+    std::memset(&s, 0, sizeof(s));
+    s.u = u_buf(par);
+    s.na = 0;
+    for (int j = 0; j < i; ++j) {
+      if (a[i][j] == 0.0) continue;  // solver.hpp:58
+      s.ka[s.na] = k_buf(j, par);
+      s.ca[s.na] = a[i][j];
+      ++s.na;
+    }
+    s.is_last = (!rhs_only && i == stages - 1) ? 1 : 0;
+    s.nb = 0;
+    if (s.is_last) {
+      for (int j = 0; j < i; ++j) {
+        if (b[j] == 0.0) continue;  // solver.hpp:71
+        s.kb[s.nb] = k_buf(j, par);
+        s.cb[s.nb] = b[j];
+        ++s.nb;
+      }
+      s.b_last = b[i];
+      s.out = out_buf(par);
+    } else {
+      s.out = k_buf(i, par);
+    }
+    s.ctl = c;
+    s.rhs_only = rhs_only ? 1 : 0;
+    s.phase = ndgx::kPhaseStage0 + i;
+    s.scan_alpha = (s.is_last && kind == NDGX_EULER_ISOTHERMAL) ? 1 : 0;
+    for (int d = 0; d < 3; ++d) {
+      s.cells[d] = cells[d];
+      s.gcells[d] = cells[d];
+      s.goff[d] = 0;
+      s.vel[d] = p.velocity[d];
+      s.lift[d] = lift[d];
+      for (int q = 0; q < 64; ++q) s.K[d][q] = K[d][q];
+    }
+    s.sound_speed = p.sound_speed;
+    return s;
+  }
+
+  void launch_stage(const StageArgs& s) const {
+    const int ntx = (cells[0] + kern.te - 1) / kern.te;
+    const long long grid = (long long)ntx * cells[1] * cells[2];
+    const int smem = s.is_last ? kern.smem_last : kern.smem_base;
+    kern.fn<<<(unsigned)grid, kern.threads, smem, stream>>>(s);
+  }
+
+  StepParams step_params(Control* c, long long fixed, int warmup) const {
+    StepParams sp;
+    sp.ctl = c;
+    sp.fixed_steps = fixed;
+    sp.t_end = p.t_end;
+    sp.cflh = cflh;
+    sp.two_n_minus_1 = two_n_minus_1;
+    sp.const_alpha = const_alpha;
+    sp.warmup = warmup;
+    return sp;
+  }
+
+  void launch_step(const StepParams& sp, int par, Control* c) const {
+    ndgx::step_begin_kernel<<<1, 1, 0, stream>>>(sp);
+    for (int i = 0; i < stages; ++i) launch_stage(stage_args(i, par, c, false));
+  }
+
+  void launch_scan(Control* c, int par) const {
+    if (kind != NDGX_EULER_ISOTHERMAL) return;
+    const int threads = 256, blocks = 148 * 8;
+    if (dim == 2)
+      ndgx::alpha_scan_kernel<2><<<blocks, threads, 0, stream>>>(u_buf(par), cells[0], cells[1], cells[2], N,
+                                                                 p.sound_speed, c, 1);
+    else
+      ndgx::alpha_scan_kernel<3><<<blocks, threads, 0, stream>>>(u_buf(par), cells[0], cells[1], cells[2], N,
+                                                                 p.sound_speed, c, 1);
+  }
+
+  void reset_control(Control* c) const {
+    Control h;
+    std::memset(&h, 0, sizeof(h));
+    h.err_key = ndgx::kNoError;
+    h.dt_min = std::numeric_limits<double>::infinity();
+    h.dt_max = 0.0;
+    *h_ctl = h;
+    ck(cudaMemcpyAsync(c, h_ctl, sizeof(Control), cudaMemcpyHostToDevice, stream), "reset control");
+  }
+
+  Control read_control(Control* c) const {
+    ck(cudaMemcpyAsync(h_ctl, c, sizeof(Control), cudaMemcpyDeviceToHost, stream), "read control");
+    ck(cudaStreamSynchronize(stream), "sync");
+    return *h_ctl;
+  }
+
+  void ensure_graphs(long long fixed) {
+    if (graph[0] && graph_fixed == fixed && graph_tend == p.t_end) return;
+    for (auto& g : graph)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+    const StepParams sp = step_params(ctl, fixed, 0);
+    for (int par = 0; par < 2; ++par) {
+      cudaGraph_t g;
+      ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+      launch_step(sp, par, ctl);
+      launch_step(sp, 1 - par, ctl);
+      ck(cudaStreamEndCapture(stream, &g), "end capture");
+      ck(cudaGraphInstantiate(&graph[par], g, 0), "graph instantiate");
+      cudaGraphDestroy(g);
+    }
+    graph_fixed = fixed;
+    graph_tend = p.t_end;
+  }
+
+  // device index of (AoS cell index, AoS node key, var)
+  size_t device_index(long long aos_cell, int aos_node, int var) const {
+    const int c2 = cells[2], c1 = cells[1];
+    const int cz = (int)(aos_cell % c2);
+    const int cy = (int)((aos_cell / c2) % c1);
+    const int cx = (int)(aos_cell / ((long long)c2 * c1));
+    int i = 0, j = 0, k = 0;
+    if (dim == 1) i = aos_node;
+    if (dim == 2) { i = aos_node / N; j = aos_node % N; }
+    if (dim == 3) { i = aos_node / (N * N); j = (aos_node / N) % N; k = aos_node % N; }
+    const size_t e = (size_t)cx + (size_t)cells[0] * ((size_t)cy + (size_t)c1 * cz);
+    const size_t nn = (size_t)i + (size_t)N * ((size_t)j + (size_t)N * k);
+    return (e * nv + var) * npe + nn;
+  }
+
+  double fetch(const double* dev, size_t idx) const {
+    double v = 0.0;
+    ck(cudaMemcpy(&v, dev + idx, sizeof(double), cudaMemcpyDeviceToHost), "fetch");
+    return v;
+  }
+
+  // Map a device error key onto the reference's exception (message text
+  // follows src/solver.cpp:258-261, 325-328, 364-365, 411-413).
+  int report(unsigned long long key, int start_par, ndgx_error* err) const {
+    const long step = (long)(key >> 44);
+    const int phase = (int)((key >> 40) & 0xF);
+    const long long cell = (long long)((key >> 12) & 0xFFFFFFF);
+    const int node = (int)(key & 0xFFF);
+    const int par = start_par ^ (int)((step > 0 ? step - 1 : 0) & 1);
+    if (phase == ndgx::kPhaseZeroSpeed) {
+      set_error(err, NDGX_ERR_CONFIG, "fixed-step run requires a positive wavespeed", step);
+      return NDGX_ERR_CONFIG;
+    }
+    if (phase == ndgx::kPhaseInstability) {
+      set_error(err, NDGX_ERR_INSTABILITY, "non-finite state after step " + std::to_string(step), step);
+      return NDGX_ERR_INSTABILITY;
+    }
+    const size_t idx = device_index(cell, node, 0);
+    if (phase == ndgx::kPhaseScan) {
+      const double rho = fetch(u_buf(par), idx);
+      set_error(err, NDGX_ERR_PHYSICS, "nonpositive density " + fmt_double(rho) + " in time-step estimate",
+                step);
+      return NDGX_ERR_PHYSICS;
+    }
+    // operator PhysicsError at stage `stage`: recompute the stage input there
+    const int stage = phase - ndgx::kPhaseStage0;
+    double rho = fetch(u_buf(par), idx);
+    for (int j = 0; j < stage; ++j) {
+      if (a[stage][j] == 0.0) continue;
+      rho += a[stage][j] * fetch(k_buf(j, par), idx);
+    }
+    int c[3];
+    c[2] = (int)(cell % cells[2]);
+    c[1] = (int)((cell / cells[2]) % cells[1]);
+    c[0] = (int)(cell / ((long long)cells[2] * cells[1]));
+    const std::string where = "(" + std::to_string(c[0]) + "," + std::to_string(c[1]) + "," +
+                              std::to_string(c[2]) + ")";
+    set_error(err, NDGX_ERR_PHYSICS,
+              "nonpositive density " + fmt_double(rho) + " in flux evaluation at cell " + where, step,
+              stage, c);
+    return NDGX_ERR_PHYSICS;
+  }
+
+  ~ndgx_solver() {
+    for (auto& g : graph)
+      if (g) cudaGraphExecDestroy(g);
+    for (double* q : buf) cudaFree(q);
+    if (ctl) cudaFree(ctl);
+    if (ctl_warm) cudaFree(ctl_warm);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+int cuda_error(ndgx_error* err, const CudaFailure& f) {
+  set_error(err, NDGX_ERR_CUDA, std::string(f.what) + ": " + cudaGetErrorString(f.rc));
+  return NDGX_ERR_CUDA;
+}
+
+int validate_problem(const ndgx_problem* p, ndgx_error* err) {
+  auto cfg = [&](const std::string& m) {
+    set_error(err, NDGX_ERR_CONFIG, m);
+    return (int)NDGX_ERR_CONFIG;
+  };
+  // Mesh ctor (src/grid.cpp:52-64)
+  if (p->dim < 1 || p->dim > 3) return cfg("mesh dimension must be 1..3");
+  if (p->order < 2 || p->order > 16) return cfg("mesh order must lie in 2..16");
+  for (int a = 0; a < p->dim; ++a) {
+    if (p->cells[a] < 1) return cfg("cell count must be >= 1 on every axis");
+    if (!(p->length[a] > 0.0)) return cfg("domain length must be positive");
+  }
+  // EquationModel factories (src/models.cpp:14-33)
+  if (p->equation == NDGX_ADVECTION) {
+  } else if (p->equation == NDGX_EULER_ISOTHERMAL) {
+    if (p->dim < 2) return cfg("isothermal_euler: spatial_dim must be 2 or 3");
+    if (!(p->sound_speed > 0.0)) return cfg("isothermal_euler: sound speed must be positive");
+  } else {
+    return cfg("unknown equation kind");
+  }
+  if (p->rk < NDGX_RK3 || p->rk > NDGX_RK6)
+    return cfg("unknown Runge-Kutta scheme (expected rk3, rk4 or rk6)");
+  // validate (src/solver.cpp:349-357)
+  if (!(p->cfl > 0.0) || p->cfl > 1.0) return cfg("cfl must lie in (0, 1]");
+  if (!(p->t_end > 0.0)) return cfg("t_end must be positive");
+  if (p->order > ndgx::kMaxOrder)
+    return cfg("the GPU path supports orders 2..8 (got " + std::to_string(p->order) + ")");
+  return NDGX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ndgx_version(void) { return "ndgx 0.1.0 sm_100a"; }
+
+int ndgx_create(const ndgx_problem* prob, ndgx_solver** out, ndgx_error* err) {
+  clear_error(err);
+  if (!prob || !out) {
+    set_error(err, NDGX_ERR_CONFIG, "null argument");
+    return NDGX_ERR_CONFIG;
+  }
+  *out = nullptr;
+  if (int rc = validate_problem(prob, err)) return rc;
+  ndgx_solver* s = new (std::nothrow) ndgx_solver();
+  if (!s) {
+    set_error(err, NDGX_ERR_CUDA, "host allocation failed");
+    return NDGX_ERR_CUDA;
+  }
+  try {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      delete s;
+      set_error(err, NDGX_ERR_CUDA, "no CUDA device: the ndgx path has no CPU fallback");
+      return NDGX_ERR_CUDA;
+    }
+    ck(cudaSetDevice(prob->device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, prob->device), "cudaGetDeviceProperties");
+    if (prop.major != 10) {
+      delete s;
+      set_error(err, NDGX_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100 (B200)");
+      return NDGX_ERR_CUDA;
+    }
+    s->p = *prob;
+    s->p.nodes = s->p.weights = s->p.diff = nullptr;
+    s->dim = prob->dim;
+    s->N = prob->order;
+    s->kind = prob->equation;
+    s->nv = s->kind == NDGX_ADVECTION ? 1 : s->dim + 1;
+    s->exact = prob->arith != NDGX_ARITH_FAST;
+    for (int a = 0; a < 3; ++a) s->cells[a] = a < s->dim ? prob->cells[a] : 1;
+    s->npe = 1;
+    for (int a = 0; a < s->dim; ++a) s->npe *= s->N;
+    s->n = (size_t)s->nv * s->npe * s->cells[0] * s->cells[1] * s->cells[2];
+    s->dof = (int64_t)s->n;
+
+    // basis: caller's (reference) or our own restatement
+    double nodes[16], weights[16], diff[256];
+    if (prob->nodes && prob->weights && prob->diff) {
+      std::memcpy(nodes, prob->nodes, sizeof(double) * s->N);
+      std::memcpy(weights, prob->weights, sizeof(double) * s->N);
+      std::memcpy(diff, prob->diff, sizeof(double) * s->N * s->N);
+    } else {
+      ndgx_gauss_lobatto(s->N, nodes, weights);
+      ndgx_differentiation_matrix(s->N, nodes, diff);
+    }
+    ndgx::build_operator(&s->p, nodes, weights, diff, s->K, s->lift);
+    ndgx::rk_tableau(prob->rk, &s->stages, s->a, s->b);
+    s->cflh = ndgx::dt_numerator(&s->p);
+    s->two_n_minus_1 = (double)(2 * s->N - 1);
+    if (s->kind == NDGX_ADVECTION) {
+      double alpha = 0.0;  // max_wavespeed_bound, advection (src/solver.cpp:312-317)
+      for (int d = 0; d < s->dim; ++d) {
+        const double v = std::abs(prob->velocity[d]);
+        alpha = (alpha < v) ? v : alpha;
+      }
+      s->const_alpha = alpha;
+    }
+    const int last = s->stages - 1;
+    s->dead = -1;
+    for (int j = 0; j < last; ++j)
+      if (s->a[last][j] == 0.0) {
+        s->dead = j;
+        break;
+      }
+
+    s->kern = ndgx::find_stage_kernel(s->dim, s->N, s->kind, s->exact);
+    if (!s->kern.fn) {
+      delete s;
+      set_error(err, NDGX_ERR_CONFIG, "no GPU kernel for this (dim, order, equation)");
+      return NDGX_ERR_CONFIG;
+    }
+    ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(s->kern.fn),
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, s->kern.smem_last),
+       "smem attribute");
+    ck(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreate(&s->ev0), "event");
+    ck(cudaEventCreate(&s->ev1), "event");
+    const int nbuf = s->dead >= 0 ? s->stages : s->stages + 1;
+    for (int q = 0; q < nbuf; ++q) {
+      double* d = nullptr;
+      ck(cudaMalloc(&d, s->n * sizeof(double)), "cudaMalloc state");
+      s->buf.push_back(d);
+    }
+    ck(cudaMemsetAsync(s->buf[0], 0, s->n * sizeof(double), s->stream), "memset");
+    ck(cudaMalloc(&s->ctl, sizeof(Control)), "cudaMalloc control");
+    ck(cudaMalloc(&s->ctl_warm, sizeof(Control)), "cudaMalloc control");
+    ck(cudaMallocHost(&s->h_ctl, sizeof(Control)), "cudaMallocHost");
+    ck(cudaStreamSynchronize(s->stream), "sync");
+  } catch (const CudaFailure& f) {
+    delete s;
+    return cuda_error(err, f);
+  }
+  *out = s;
+  return NDGX_OK;
+}
+
+void ndgx_destroy(ndgx_solver* s) {
+  if (!s) return;
+  cudaSetDevice(s->p.device);
+  cudaStreamSynchronize(s->stream);
+  delete s;
+}
+
+int64_t ndgx_dof(const ndgx_solver* s) { return s ? s->dof : 0; }
+size_t ndgx_state_size(const ndgx_solver* s) { return s ? s->n : 0; }
+int ndgx_stages(const ndgx_solver* s) { return s ? s->stages : 0; }
+void* ndgx_stream(ndgx_solver* s) { return s ? (void*)s->stream : nullptr; }
+
+static void permute(const ndgx_solver* s, const double* src, double* dst, bool to_device) {
+  const long long total = (long long)s->n;
+  const int threads = 256;
+  const int blocks = (int)std::min<long long>((total + threads - 1) / threads, 148LL * 16);
+  if (to_device)
+    ndgx::permute_kernel<true><<<blocks, threads, 0, s->stream>>>(src, dst, s->dim, s->cells[0], s->cells[1],
+                                                                  s->cells[2], s->N, s->nv, total);
+  else
+    ndgx::permute_kernel<false><<<blocks, threads, 0, s->stream>>>(src, dst, s->dim, s->cells[0], s->cells[1],
+                                                                   s->cells[2], s->N, s->nv, total);
+}
+
+int ndgx_upload(ndgx_solver* s, const double* u_aos, ndgx_error* err) {
+  clear_error(err);
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    double* st = s->staging(s->parity);
+    ck(cudaMemcpyAsync(st, u_aos, s->n * sizeof(double), cudaMemcpyHostToDevice, s->stream), "upload");
+    permute(s, st, s->u_buf(s->parity), true);
+    ck(cudaGetLastError(), "permute launch");
+    ck(cudaStreamSynchronize(s->stream), "upload sync");
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+  return NDGX_OK;
+}
+
+int ndgx_download(ndgx_solver* s, double* u_aos, ndgx_error* err) {
+  clear_error(err);
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    double* st = s->staging(s->parity);
+    permute(s, s->u_buf(s->parity), st, false);
+    ck(cudaGetLastError(), "permute launch");
+    ck(cudaMemcpyAsync(u_aos, st, s->n * sizeof(double), cudaMemcpyDeviceToHost, s->stream), "download");
+    ck(cudaStreamSynchronize(s->stream), "download sync");
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+  return NDGX_OK;
+}
+
+int ndgx_rhs(ndgx_solver* s, double* dudt_aos, ndgx_error* err) {
+  clear_error(err);
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    s->reset_control(s->ctl_warm);
+    const StageArgs a = s->stage_args(0, s->parity, s->ctl_warm, true);
+    s->launch_stage(a);
+    ck(cudaGetLastError(), "rhs launch");
+    const Control c = s->read_control(s->ctl_warm);
+    if (c.err_key != ndgx::kNoError) return s->report(c.err_key, s->parity, err);
+    double* st = s->staging(s->parity);
+    permute(s, a.out, st, false);
+    ck(cudaMemcpyAsync(dudt_aos, st, s->n * sizeof(double), cudaMemcpyDeviceToHost, s->stream), "download");
+    ck(cudaStreamSynchronize(s->stream), "rhs sync");
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+  return NDGX_OK;
+}
+
+static int run_warmup(ndgx_solver* s, ndgx_error* err) {
+  // one untimed step on a scratch copy (src/solver.cpp:397-403): u itself is
+  // never written by a step (u_new goes to the other parity buffer)
+  s->reset_control(s->ctl_warm);
+  s->launch_scan(s->ctl_warm, s->parity);
+  s->launch_step(s->step_params(s->ctl_warm, 1, 1), s->parity, s->ctl_warm);
+  ck(cudaGetLastError(), "warmup launch");
+  const Control c = s->read_control(s->ctl_warm);
+  if (c.err_key != ndgx::kNoError) {
+    const int phase = (int)((c.err_key >> 40) & 0xF);
+    const long step = (long)(c.err_key >> 44);
+    // the warm-up has no finite check and no trailing scan
+    if (phase != ndgx::kPhaseInstability && !(phase == ndgx::kPhaseScan && step > 1))
+      return s->report(c.err_key, s->parity, err);
+  }
+  return NDGX_OK;
+}
+
+static int finish_run(ndgx_solver* s, long long fixed, int start_par, ndgx_stats* stats, ndgx_error* err) {
+  ck(cudaEventRecord(s->ev1, s->stream), "event");
+  const Control c = s->read_control(s->ctl);
+  float ms = 0.0f;
+  ck(cudaEventElapsedTime(&ms, s->ev0, s->ev1), "elapsed");
+  if (c.err_key != ndgx::kNoError) {
+    const long step = (long)(c.err_key >> 44);
+    const int phase = (int)((c.err_key >> 40) & 0xF);
+    bool real = true;
+    if (phase == ndgx::kPhaseScan && step > 1) {
+      // scan of the state after step-1: only real if that step was followed by another
+      if (fixed >= 0) real = step <= fixed;
+      else real = !c.done && c.t < s->p.t_end;
+    }
+    if (real) {
+      s->parity = start_par;  // state undefined after an exception; keep the input
+      return s->report(c.err_key, start_par, err);
+    }
+  }
+  s->parity = start_par ^ (int)(c.steps & 1);
+  if (stats) {
+    stats->steps = (long)c.steps;
+    stats->dt_min = c.dt_min;
+    stats->dt_max = c.dt_max;
+    stats->wall_seconds = ms * 1e-3;
+  }
+  return NDGX_OK;
+}
+
+int ndgx_advance(ndgx_solver* s, long fixed_steps, int warmup, ndgx_stats* stats, ndgx_error* err) {
+  clear_error(err);
+  if (stats) {
+    stats->steps = 0;
+    stats->dt_min = std::numeric_limits<double>::infinity();
+    stats->dt_max = 0.0;
+    stats->wall_seconds = 0.0;
+  }
+  if (!(s->p.cfl > 0.0) || s->p.cfl > 1.0) {
+    set_error(err, NDGX_ERR_CONFIG, "cfl must lie in (0, 1]");
+    return NDGX_ERR_CONFIG;
+  }
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    if (warmup) {
+      if (int rc = run_warmup(s, err)) return rc;
+    }
+    const long long fixed = fixed_steps >= 0 ? fixed_steps : -1;
+    s->ensure_graphs(fixed);
+    const int start_par = s->parity;
+    s->reset_control(s->ctl);
+    ck(cudaEventRecord(s->ev0, s->stream), "event");
+    s->launch_scan(s->ctl, start_par);
+    if (fixed >= 0) {
+      // pairs of steps alternate the parity; a trailing odd step is skipped
+      // on the device by step_begin (steps >= fixed_steps)
+      for (long long q = 0; q < (fixed + 1) / 2; ++q) ck(cudaGraphLaunch(s->graph[start_par], s->stream), "graph");
+    } else {
+      // t_end: the device decides when to stop; poll every chunk of steps
+      const int chunk = 8;  // graph launches (2 steps each) between polls
+      for (;;) {
+        for (int q = 0; q < chunk; ++q) ck(cudaGraphLaunch(s->graph[start_par], s->stream), "graph");
+        const Control c = s->read_control(s->ctl);
+        if (c.done || c.err_key != ndgx::kNoError) break;
+      }
+    }
+    return finish_run(s, fixed, start_par, stats, err);
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+}
+
+int ndgx_launch_steps(ndgx_solver* s, long steps, ndgx_error* err) {
+  clear_error(err);
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    const long long fixed = steps;
+    s->ensure_graphs(fixed);
+    s->pending_start_parity = s->parity;
+    s->pending_fixed = fixed;
+    s->reset_control(s->ctl);
+    ck(cudaEventRecord(s->ev0, s->stream), "event");
+    s->launch_scan(s->ctl, s->parity);
+    for (long long q = 0; q < (fixed + 1) / 2; ++q) ck(cudaGraphLaunch(s->graph[s->parity], s->stream), "graph");
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+  return NDGX_OK;
+}
+
+int ndgx_sync(ndgx_solver* s, ndgx_stats* stats, ndgx_error* err) {
+  clear_error(err);
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    if (s->pending_fixed < 0) {
+      ck(cudaStreamSynchronize(s->stream), "sync");
+      return NDGX_OK;
+    }
+    const long long fixed = s->pending_fixed;
+    s->pending_fixed = -1;
+    return finish_run(s, fixed, s->pending_start_parity, stats, err);
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+}
+
+int ndgx_profile_step(ndgx_solver* s, float* ms, int n, ndgx_error* err) {
+  clear_error(err);
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    std::vector<cudaEvent_t> ev(s->stages + 3);
+    for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    s->reset_control(s->ctl_warm);
+    s->launch_scan(s->ctl_warm, s->parity);
+    ck(cudaEventRecord(ev[0], s->stream), "event");
+    ndgx::step_begin_kernel<<<1, 1, 0, s->stream>>>(s->step_params(s->ctl_warm, 1, 0));
+    ck(cudaEventRecord(ev[1], s->stream), "event");
+    for (int i = 0; i < s->stages; ++i) {
+      s->launch_stage(s->stage_args(i, s->parity, s->ctl_warm, false));
+      ck(cudaEventRecord(ev[2 + i], s->stream), "event");
+    }
+    ck(cudaStreamSynchronize(s->stream), "sync");
+    for (int i = 0; i < s->stages && i < n; ++i) ck(cudaEventElapsedTime(&ms[i], ev[1 + i], ev[2 + i]), "elapsed");
+    if (s->stages < n) ck(cudaEventElapsedTime(&ms[s->stages], ev[0], ev[1]), "elapsed");
+    for (auto& e : ev) cudaEventDestroy(e);
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+  return NDGX_OK;
+}
+
+}  // extern "C"
+
+namespace ndgx {
+StageKernel find_stage_kernel(int dim, int order, int kind, bool exact) {
+  if (dim == 1) return find_stage_kernel_d1(order, kind, exact);
+  if (dim == 2) return find_stage_kernel_d2(order, kind, exact);
+  if (dim == 3) return find_stage_kernel_d3(order, kind, exact);
+  return StageKernel{};
+}
+}  // namespace ndgx
