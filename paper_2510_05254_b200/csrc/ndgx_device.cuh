@@ -74,14 +74,16 @@ struct StepParams {
 
 struct StageArgs {
   const double* u;                 // u^n
-  const double* ka[kMaxTerms];     // stage-input terms (ascending j, a_sj != 0)
+  // union of the K_j read by this stage (ascending j): the stage input uses
+  // those with bit t of amask (coefficient ca[t] = a_sj != 0), the last
+  // stage's S = u + sum b_j K_j those with bit t of bmask (cb[t] = b_j != 0)
+  const double* ku[kMaxTerms];
   double ca[kMaxTerms];
-  const double* kb[kMaxTerms];     // last stage: S = u + sum b_j K_j (ascending j, b_j != 0)
   double cb[kMaxTerms];
+  int nu, amask, bmask;
   double* out;                     // K_s, or u_new at the last stage
   Control* ctl;
   double b_last;
-  int na, nb;
   int is_last;
   int rhs_only;                    // serial_rhs: dt := 1, no step control
   int phase;                       // kPhaseStage0 + stage
@@ -123,24 +125,38 @@ struct Ar<false> {  // contracted
 
 __device__ __forceinline__ double dmax(double a, double b) { return (a < b) ? b : a; }
 
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+
 template <int DIM, int N, int KIND>
 struct Geo {
   static constexpr int NV = (KIND == 0) ? 1 : DIM + 1;
-  static constexpr int L = (DIM == 1) ? 1 : (DIM == 2 ? N : N * N);  // lines per element
+  static constexpr int L = (DIM == 1) ? 1 : (DIM == 2 ? N : N * N);  // lines per element per axis
   static constexpr int NPE = L * N;                                   // nodes per element
-  static constexpr int NPEP = L * (N + 1);  // padded shared-memory element stride
-  static constexpr int TE = (128 / L) < 1 ? 1 : (128 / L);            // elements per tile
+  static constexpr int LP = L * (N + 1);  // padded shared-memory stride of one element variable
+  // element tile TX x TY x TZ (powers of two), ~128 line-owner threads
+  static constexpr int TE = 1 << ilog2((128 / L) < 1 ? 1 : (128 / L));
+  static constexpr int LG = ilog2(TE);
+  static constexpr int LX = DIM == 1 ? LG : (DIM == 2 ? (LG + 1) / 2 : (LG + 2) / 3);
+  static constexpr int LY = DIM == 1 ? 0 : (DIM == 2 ? LG - LX : (LG - LX + 1) / 2);
+  static constexpr int LZ = LG - LX - LY;
+  static constexpr int TX = 1 << LX, TY = 1 << LY, TZ = 1 << LZ;
   static constexpr int THREADS = TE * L;
-  static constexpr int ARR = TE * NV * NPEP;  // doubles in one shared field tile
-  static constexpr int TRC = TE * 2 * NV * L; // doubles in one axis' trace buffer
-  // shared memory carve-up (doubles): F[1..DIM-1], P, traces[DIM], red[32], S (last stage)
-  static constexpr int OFF_F = 0;
-  static constexpr int OFF_P = OFF_F + (DIM - 1) * ARR;
-  static constexpr int OFF_T = OFF_P + (DIM > 1 ? ARR : 0);
-  static constexpr int OFF_R = OFF_T + DIM * TRC;
-  static constexpr int OFF_S = OFF_R + 32;
+  static constexpr int PAIR = (N % 2 == 0) ? 2 : 1;  // doubles per prepass load
+  // halo faces per tile side along axis d = TE / T_d
+  static constexpr int HF0 = TE / TX, HF1 = TE / TY, HF2 = TE / TZ;
+  static constexpr int HOFF1 = 2 * HF0 * NV * L;
+  static constexpr int HOFF2 = HOFF1 + (DIM > 1 ? 2 * HF1 * NV * L : 0);
+  static constexpr int HSIZE = HOFF2 + (DIM > 2 ? 2 * HF2 * NV * L : 0);
+  // shared memory carve-up (doubles)
+  static constexpr int ARR = TE * NV * LP;
+  static constexpr int OFF_U = 0;                           // U_s, later the partial dudt P
+  static constexpr int OFF_F = OFF_U + ARR;                 // F_axis for axes 1..DIM-1
+  static constexpr int OFF_T = OFF_F + (DIM - 1) * ARR;     // own U traces, axes 1..DIM-1
+  static constexpr int OFF_H = OFF_T + (DIM - 1) * TE * 2 * NV * L;  // out-of-tile halo U_s
+  static constexpr int OFF_R = OFF_H + HSIZE;               // reduction scratch
+  static constexpr int OFF_S = OFF_R + 32;                  // S (last stage)
   static constexpr int SMEM_BASE = OFF_S * 8;
-  static constexpr int SMEM_LAST = (OFF_S + (DIM > 1 ? ARR : 0)) * 8;
+  static constexpr int SMEM_LAST = (OFF_S + ARR) * 8;
 
   // node index of position k along `axis` for transverse line index tr
   static __device__ __forceinline__ int node(int axis, int tr, int k) {
@@ -148,8 +164,9 @@ struct Geo {
     if (axis == 1) return (tr % N) + N * (k + N * (tr / N));
     return tr + N * N * k;
   }
-  // padded shared-memory slot of node n (x-lines padded to N+1: conflict-free
-  // for both x-line owners and y/z-line owners)
+  // padded shared-memory slot of node n: x-lines padded to N+1 doubles, so
+  // x-line owners (lane stride N+1) and y/z-line owners (unit stride) are
+  // both bank-conflict free
   static __device__ __forceinline__ int sn(int n) { return n + n / N; }
   // AoS node order inside a cell (grid.hpp:50-56): i slowest
   static __device__ __forceinline__ int aos_node(int n) {
@@ -158,6 +175,12 @@ struct Geo {
     const int j = (n / N) % N;
     if (DIM == 2) return i * N + j;
     return (i * N + j) * N + n / (N * N);
+  }
+  static __device__ __forceinline__ int halo_off(int axis) {
+    return axis == 0 ? 0 : (axis == 1 ? HOFF1 : HOFF2);
+  }
+  static __device__ __forceinline__ int halo_faces(int axis) {
+    return axis == 0 ? HF0 : (axis == 1 ? HF1 : HF2);
   }
 };
 
@@ -193,15 +216,6 @@ __device__ __forceinline__ void lax_friedrichs(const double* um, const double* u
     fhat[v] = A::mul(0.5, A::sub(A::add(fm[v], fp[v]), A::mul(alpha, A::sub(up[v], um[v]))));
 }
 
-// Stage input at one global index: stage_ = u; stage_ += a_sj k_j (solver.hpp:55-62).
-template <bool EXACT>
-__device__ __forceinline__ double stage_input(const StageArgs& p, size_t idx) {
-  using A = Ar<EXACT>;
-  double s = __ldg(p.u + idx);
-  for (int t = 0; t < p.na; ++t) s = A::mac(s, p.ca[t], __ldg(p.ka[t] + idx));
-  return s;
-}
-
 __device__ __forceinline__ void record_error(Control* ctl, unsigned long long key) {
   if (key < *(volatile unsigned long long*)&ctl->err_key) atomicMin(&ctl->err_key, key);
 }
@@ -212,13 +226,164 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// 0 + x as the reference's dudt.assign(0) followed by out += acc: x, except
+// -0 becomes +0.  Done on the integer pipe instead of a DADD.
+__device__ __forceinline__ double zero_plus(double x) {
+  const long long b = __double_as_longlong(x);
+  return (b << 1) == 0 ? 0.0 : x;
+}
+
+template <int PAIR>
+struct Vec;
+template <>
+struct Vec<1> {
+  double x;
+  static __device__ __forceinline__ Vec ld(const double* p) { return Vec{__ldg(p)}; }
+};
+template <>
+struct Vec<2> {
+  double x, y;
+  static __device__ __forceinline__ Vec ld(const double* p) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    return Vec{v.x, v.y};
+  }
+};
+
+// Tile geometry shared by the prepass and the line phases.
+struct TileCtx {
+  int x0, y0, z0;     // tile origin (cells)
+  int vx, vy, vz;     // valid extent of the tile along each axis
+};
+
+// ------------------------------------------------------------ prepass
+// Node-parallel, coalesced, all terms in flight: U_s = u + sum a_sj K_j and
+// (last stage) S = u + sum b_j K_j for every node of the tile, into padded
+// shared memory; then the out-of-tile neighbours' face planes into the halo.
+template <int DIM, int N, int KIND, bool EXACT, int NU>
+__device__ __forceinline__ void prepass(const StageArgs& p, const TileCtx& tc, double* smem) {
+  using G = Geo<DIM, N, KIND>;
+  using A = Ar<EXACT>;
+  constexpr int NV = G::NV, NPE = G::NPE, LP = G::LP, TE = G::TE, PAIR = G::PAIR;
+  constexpr int PER_EL = NV * NPE / PAIR;  // items per element
+  constexpr int ITEMS = TE * PER_EL;
+  // ~8 double2 loads in flight per thread whatever the number of terms
+  constexpr int UNR = (8 / (1 + NU)) < 1 ? 1 : ((8 / (1 + NU)) > 4 ? 4 : 8 / (1 + NU));
+  const int T = blockDim.x;
+  const int C0 = p.cells[0], C1 = p.cells[1];
+  double* sU = smem + G::OFF_U;
+  double* sS = smem + G::OFF_S;
+  const bool last = p.is_last;
+
+  for (int base = threadIdx.x; base < ITEMS; base += UNR * T) {
+    Vec<PAIR> uu[UNR], kk[UNR][NU > 0 ? NU : 1];
+    size_t gaddr[UNR];
+    int saddr[UNR];
+    bool ok[UNR];
+#pragma unroll
+    for (int w = 0; w < UNR; ++w) {
+      const int q = base + w * T;
+      const int el = q / PER_EL;
+      const int r = (q - el * PER_EL) * PAIR;
+      const int ex = el % G::TX, ey = (el / G::TX) % G::TY, ez = el / (G::TX * G::TY);
+      ok[w] = q < ITEMS && ex < tc.vx && ey < tc.vy && ez < tc.vz;
+      const size_t e = (size_t)(tc.x0 + ex) + (size_t)C0 * ((size_t)(tc.y0 + ey) + (size_t)C1 * (tc.z0 + ez));
+      gaddr[w] = e * NV * NPE + r;
+      const int v = r / NPE, n = r - v * NPE;
+      saddr[w] = (el * NV + v) * LP + G::sn(n);
+      if (ok[w]) {
+        uu[w] = Vec<PAIR>::ld(p.u + gaddr[w]);
+#pragma unroll
+        for (int t = 0; t < NU; ++t) kk[w][t] = Vec<PAIR>::ld(p.ku[t] + gaddr[w]);
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < UNR; ++w) {
+      if (!ok[w]) continue;
+      double U0 = uu[w].x, S0 = uu[w].x;
+#pragma unroll
+      for (int t = 0; t < NU; ++t) {
+        if (p.amask >> t & 1) U0 = A::mac(U0, p.ca[t], kk[w][t].x);
+        if (last && (p.bmask >> t & 1)) S0 = A::mac(S0, p.cb[t], kk[w][t].x);
+      }
+      sU[saddr[w]] = U0;
+      if (last) sS[saddr[w]] = S0;
+      if constexpr (PAIR == 2) {
+        double U1 = uu[w].y, S1 = uu[w].y;
+#pragma unroll
+        for (int t = 0; t < NU; ++t) {
+          if (p.amask >> t & 1) U1 = A::mac(U1, p.ca[t], kk[w][t].y);
+          if (last && (p.bmask >> t & 1)) S1 = A::mac(S1, p.cb[t], kk[w][t].y);
+        }
+        sU[saddr[w] + 1] = U1;  // n and n+1 share an x-line (N even)
+        if (last) sS[saddr[w] + 1] = S1;
+      }
+    }
+  }
+
+  // halo: the face plane of each out-of-tile neighbour (always loaded, also
+  // when the periodic wrap lands inside the tile -- the values are identical)
+  constexpr int L = G::L;
+  constexpr int H0 = 2 * G::HF0 * NV * L;
+  constexpr int H1 = DIM > 1 ? 2 * G::HF1 * NV * L : 0;
+  constexpr int H2 = DIM > 2 ? 2 * G::HF2 * NV * L : 0;
+  constexpr int HITEMS = H0 + H1 + H2;
+  double* sH = smem + G::OFF_H;
+  for (int base = threadIdx.x; base < HITEMS; base += 2 * T) {
+    double hu[2], hk[2][NU > 0 ? NU : 1];
+    int hdst[2];
+    bool ok[2];
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const int q = base + w * T;
+      ok[w] = q < HITEMS;
+      int axis, r;
+      if (q < H0) { axis = 0; r = q; }
+      else if (q < H0 + H1) { axis = 1; r = q - H0; }
+      else { axis = 2; r = q - H0 - H1; }
+      const int nf = axis == 0 ? G::HF0 : (axis == 1 ? G::HF1 : G::HF2);
+      // r = ((side * nf + f) * NV + v) * L + t
+      const int t = r % L;
+      const int v = (r / L) % NV;
+      const int f = (r / (L * NV)) % nf;
+      const int side = r / (L * NV * nf);
+      // tile element on the tile boundary: transverse coords from f
+      int ex, ey, ez;
+      if (axis == 0) { ey = f % G::TY; ez = f / G::TY; ex = side ? tc.vx - 1 : 0; }
+      else if (axis == 1) { ex = f % G::TX; ez = f / G::TX; ey = side ? tc.vy - 1 : 0; }
+      else { ex = f % G::TX; ey = f / G::TX; ez = side ? tc.vz - 1 : 0; }
+      ok[w] = ok[w] && ex < tc.vx && ey < tc.vy && ez < tc.vz;
+      int c[3] = {tc.x0 + ex, tc.y0 + ey, tc.z0 + ez};
+      const int cn = p.cells[axis];
+      c[axis] = side ? (c[axis] + 1 == cn ? 0 : c[axis] + 1) : (c[axis] == 0 ? cn - 1 : c[axis] - 1);
+      const size_t e = (size_t)c[0] + (size_t)C0 * ((size_t)c[1] + (size_t)C1 * c[2]);
+      const int n = G::node(axis, t, side ? 0 : N - 1);
+      const size_t g = e * NV * NPE + (size_t)v * NPE + n;
+      hdst[w] = q - (axis == 0 ? 0 : (axis == 1 ? H0 : H0 + H1)) + G::halo_off(axis);
+      if (ok[w]) {
+        hu[w] = __ldg(p.u + g);
+#pragma unroll
+        for (int tt = 0; tt < NU; ++tt) hk[w][tt] = __ldg(p.ku[tt] + g);
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      if (!ok[w]) continue;
+      double U0 = hu[w];
+#pragma unroll
+      for (int tt = 0; tt < NU; ++tt)
+        if (p.amask >> tt & 1) U0 = A::mac(U0, p.ca[tt], hk[w][tt]);
+      sH[hdst[w]] = U0;
+    }
+  }
+}
+
 // ============================================================ stage kernel
 template <int DIM, int N, int KIND, bool EXACT>
 __global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS)
 stage_kernel(const __grid_constant__ StageArgs p) {
   using G = Geo<DIM, N, KIND>;
   using A = Ar<EXACT>;
-  constexpr int NV = G::NV, L = G::L, NPE = G::NPE, NPEP = G::NPEP, TE = G::TE;
+  constexpr int NV = G::NV, L = G::L, NPE = G::NPE, LP = G::LP, TE = G::TE;
   extern __shared__ double smem[];
 
   Control* ctl = p.ctl;
@@ -229,90 +394,72 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     return;
 
   const int C0 = p.cells[0], C1 = p.cells[1], C2 = p.cells[2];
-  (void)C2;
-  const int ntx = (C0 + TE - 1) / TE;
+  const int ntx = (C0 + G::TX - 1) / G::TX, nty = (C1 + G::TY - 1) / G::TY;
   const int bid = blockIdx.x;
-  const int tx = bid % ntx;
-  const int rest = bid / ntx;
-  const int cy = rest % C1;
-  const int cz = rest / C1;
-  const int x0 = tx * TE;
-  const int nvalid = min(TE, C0 - x0);
+  TileCtx tc;
+  tc.x0 = (bid % ntx) * G::TX;
+  tc.y0 = ((bid / ntx) % nty) * G::TY;
+  tc.z0 = (bid / (ntx * nty)) * G::TZ;
+  tc.vx = min(G::TX, C0 - tc.x0);
+  tc.vy = min(G::TY, C1 - tc.y0);
+  tc.vz = min(G::TZ, C2 - tc.z0);
 
   const int tid = threadIdx.x;
   const int el = tid / L;
   const int tr = tid % L;  // transverse line index (same count for every axis)
-  const bool valid = el < nvalid;
-  const int cx = x0 + el;
+  const int ex = el % G::TX, ey = (el / G::TX) % G::TY, ez = el / (G::TX * G::TY);
+  const bool valid = ex < tc.vx && ey < tc.vy && ez < tc.vz;
+  const int cx = tc.x0 + ex, cy = tc.y0 + ey, cz = tc.z0 + ez;
   const size_t e = (size_t)cx + (size_t)C0 * ((size_t)cy + (size_t)C1 * cz);
   const size_t ebase = e * NV * NPE;
 
   const double dt = p.rhs_only ? 1.0 : ctl->dt;
   const long long step = p.rhs_only ? 0 : ctl->steps;
 
-  double* sF = smem + G::OFF_F;  // [DIM-1][TE][NV][NPEP]
-  double* sP = smem + G::OFF_P;  // [TE][NV][NPEP]
-  double* sT = smem + G::OFF_T;  // [DIM][TE][2][NV][L]
+  double* sU = smem + G::OFF_U;  // [TE][NV][LP]  U_s, then P
+  double* sF = smem + G::OFF_F;  // [DIM-1][TE][NV][LP]
+  double* sT = smem + G::OFF_T;  // [DIM-1][TE][2][NV][L]
+  double* sH = smem + G::OFF_H;  // halo
   double* sR = smem + G::OFF_R;  // [32]
-  double* sS = smem + G::OFF_S;  // [TE][NV][NPEP] (last stage, DIM > 1)
+  double* sS = smem + G::OFF_S;  // [TE][NV][LP] (last stage)
 
-  auto trc = [&](int axis, int elx, int side, int v, int t) -> double& {
-    return sT[(((axis * TE + elx) * 2 + side) * NV + v) * L + t];
-  };
   auto fld = [&](double* base, int elx, int v, int n) -> double& {
-    return base[(elx * NV + v) * NPEP + G::sn(n)];
+    return base[(elx * NV + v) * LP + G::sn(n)];
+  };
+  auto trc = [&](int axis, int elx, int side, int v, int t) -> double& {  // axis >= 1
+    return sT[((((axis - 1) * TE + elx) * 2 + side) * NV + v) * L + t];
+  };
+  auto halo = [&](int axis, int side, int f, int v, int t) -> double {
+    return sH[G::halo_off(axis) + ((side * G::halo_faces(axis) + f) * NV + v) * L + t];
   };
   auto aos_cell = [&](int x, int y, int z) -> long long {  // global AoS cell index
     const long long gx = x + p.goff[0], gy = y + p.goff[1], gz = z + p.goff[2];
     return (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz;
   };
 
+  // ---------------------------------------------------------------- prepass
+  switch (p.nu) {
+    case 0: prepass<DIM, N, KIND, EXACT, 0>(p, tc, smem); break;
+    case 1: prepass<DIM, N, KIND, EXACT, 1>(p, tc, smem); break;
+    case 2: prepass<DIM, N, KIND, EXACT, 2>(p, tc, smem); break;
+    case 3: prepass<DIM, N, KIND, EXACT, 3>(p, tc, smem); break;
+    case 4: prepass<DIM, N, KIND, EXACT, 4>(p, tc, smem); break;
+    case 5: prepass<DIM, N, KIND, EXACT, 5>(p, tc, smem); break;
+    default: prepass<DIM, N, KIND, EXACT, 6>(p, tc, smem); break;
+  }
+  __syncthreads();
+
   // ---------------------------------------------------------------- phase X
   double D[NV][N];
-  double S[NV][N];
-  double f_lo[NV], f_hi[NV], u_lo[NV], u_hi[NV];
-  double s_lo = 0.0, s_hi = 0.0;
-  (void)S;
   if (valid) {
     double U[NV][N];
-    const size_t lb = ebase + (size_t)tr * N;
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int i = 0; i < N; ++i) U[v][i] = __ldg(p.u + lb + (size_t)v * NPE + i);
-    if (p.is_last) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int i = 0; i < N; ++i) S[v][i] = U[v][i];
-    }
-    for (int t = 0; t < p.na; ++t) {
-      const double* kt = p.ka[t] + lb;
-      const double c = p.ca[t];
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int i = 0; i < N; ++i) U[v][i] = A::mac(U[v][i], c, __ldg(kt + (size_t)v * NPE + i));
-    }
-    if (p.is_last) {
-      for (int t = 0; t < p.nb; ++t) {
-        const double* kt = p.kb[t] + lb;
-        const double c = p.cb[t];
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-          for (int i = 0; i < N; ++i) S[v][i] = A::mac(S[v][i], c, __ldg(kt + (size_t)v * NPE + i));
-      }
-      if (DIM > 1) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-          for (int i = 0; i < N; ++i) fld(sS, el, v, i + N * tr) = S[v][i];
-      }
-    }
-
+      for (int i = 0; i < N; ++i) U[v][i] = fld(sU, el, v, i + N * tr);
     // fluxes at every node of the line, every axis
     double FX[NV][N];
+    double s_lo = 0.0, s_hi = 0.0;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double un[NV], f[NV], sp;
@@ -344,18 +491,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         double acc = 0.0;
 #pragma unroll
         for (int l = 0; l < N; ++l) acc = A::mac(acc, p.K[0][k * N + l], FX[v][l]);
-        D[v][k] = A::add(0.0, acc);
+        D[v][k] = zero_plus(acc);
       }
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      f_lo[v] = FX[v][0];
-      f_hi[v] = FX[v][N - 1];
-      u_lo[v] = U[v][0];
-      u_hi[v] = U[v][N - 1];
-      trc(0, el, 0, v, tr) = U[v][0];  // own x traces for in-tile neighbours
-      trc(0, el, 1, v, tr) = U[v][N - 1];
-    }
-    if (DIM > 1) {  // own y/z face traces for the later phases
+    // own y/z face traces for the later phases (sU becomes P below)
+    if (DIM > 1) {
       const int j = tr % N, k = tr / N;
       if (j == 0 || j == N - 1) {
 #pragma unroll
@@ -370,48 +509,37 @@ stage_kernel(const __grid_constant__ StageArgs p) {
           for (int v = 0; v < NV; ++v) trc(2, el, k == 0 ? 0 : 1, v, i + N * j) = U[v][i];
       }
     }
-  }
-  __syncthreads();
-
-  // x faces (solver.cpp:268-306): face at i=0 (we are its + side) and at
-  // i=N-1 (we are its - side).  The minus state is always the lower cell.
-  if (valid) {
+    // x faces (solver.cpp:268-306): face at i=0 (we are its + side) and at
+    // i=N-1 (we are its - side); the minus state is always the lower cell
     double nb_lo[NV], nb_hi[NV];
-    const int xl = (cx == 0) ? C0 - 1 : cx - 1;
-    const int xr = (cx == C0 - 1) ? 0 : cx + 1;
-    if (xl >= x0 && xl < x0 + nvalid) {
+    const int fx = ey + G::TY * ez;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) nb_lo[v] = trc(0, xl - x0, 1, v, tr);
-    } else {
-      const size_t nbase = ((size_t)xl + (size_t)C0 * ((size_t)cy + (size_t)C1 * cz)) * NV * NPE;
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-        nb_lo[v] = stage_input<EXACT>(p, nbase + (size_t)v * NPE + (N - 1) + (size_t)N * tr);
+    for (int v = 0; v < NV; ++v) {
+      nb_lo[v] = ex > 0 ? fld(sU, el - 1, v, (N - 1) + N * tr) : halo(0, 0, fx, v, tr);
+      nb_hi[v] = ex < tc.vx - 1 ? fld(sU, el + 1, v, N * tr) : halo(0, 1, fx, v, tr);
     }
-    if (xr >= x0 && xr < x0 + nvalid) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) nb_hi[v] = trc(0, xr - x0, 0, v, tr);
-    } else {
-      const size_t nbase = ((size_t)xr + (size_t)C0 * ((size_t)cy + (size_t)C1 * cz)) * NV * NPE;
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-        nb_hi[v] = stage_input<EXACT>(p, nbase + (size_t)v * NPE + (size_t)N * tr);
-    }
-    double fn[NV], sn, fhat[NV];
+    double fo[NV], fn[NV], sn, fhat[NV], uo[NV];
     const double lift = p.lift[0];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) { fo[v] = FX[v][0]; uo[v] = U[v][0]; }
     flux<DIM, KIND, EXACT>(p, nb_lo, 0, fn, sn);
-    lax_friedrichs<NV, EXACT>(nb_lo, u_lo, fn, f_lo, sn, s_lo, fhat);
+    lax_friedrichs<NV, EXACT>(nb_lo, uo, fn, fo, sn, s_lo, fhat);
 #pragma unroll
     for (int v = 0; v < NV; ++v) D[v][0] = A::add(D[v][0], A::mul(lift, fhat[v]));
+#pragma unroll
+    for (int v = 0; v < NV; ++v) { fo[v] = FX[v][N - 1]; uo[v] = U[v][N - 1]; }
     flux<DIM, KIND, EXACT>(p, nb_hi, 0, fn, sn);
-    lax_friedrichs<NV, EXACT>(u_hi, nb_hi, f_hi, fn, s_hi, sn, fhat);
+    lax_friedrichs<NV, EXACT>(uo, nb_hi, fo, fn, s_hi, sn, fhat);
 #pragma unroll
     for (int v = 0; v < NV; ++v) D[v][N - 1] = A::sub(D[v][N - 1], A::mul(lift, fhat[v]));
-    if (DIM > 1) {
+  }
+  if (DIM > 1) {
+    __syncthreads();  // every x-face read of sU is done: sU becomes P
+    if (valid) {
 #pragma unroll
       for (int v = 0; v < NV; ++v)
 #pragma unroll
-        for (int i = 0; i < N; ++i) fld(sP, el, v, i + N * tr) = D[v][i];
+        for (int i = 0; i < N; ++i) fld(sU, el, v, i + N * tr) = D[v][i];
     }
   }
 
@@ -433,36 +561,20 @@ stage_kernel(const __grid_constant__ StageArgs p) {
           double acc = 0.0;
 #pragma unroll
           for (int l = 0; l < N; ++l) acc = A::mac(acc, p.K[axis][k * N + l], F[v][l]);
-          D[v][k] = A::add(fld(sP, el, v, G::node(axis, tr, k)), acc);
+          D[v][k] = A::add(fld(sU, el, v, G::node(axis, tr, k)), acc);
         }
-      // faces along this axis
+      // faces along this axis: own traces, neighbours from the tile or the halo
+      const int ea = axis == 1 ? ey : ez;
+      const int va = axis == 1 ? tc.vy : tc.vz;
+      const int step_el = axis == 1 ? G::TX : G::TX * G::TY;
+      const int fidx = axis == 1 ? ex + G::TX * ez : ex + G::TX * ey;
       double a_lo[NV], a_hi[NV], nb_lo[NV], nb_hi[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         a_lo[v] = trc(axis, el, 0, v, tr);
         a_hi[v] = trc(axis, el, 1, v, tr);
-      }
-      const int cn = p.cells[axis];
-      const int ca = (axis == 1) ? cy : cz;
-      const int lo_c = (ca == 0) ? cn - 1 : ca - 1;
-      const int hi_c = (ca == cn - 1) ? 0 : ca + 1;
-      if (cn == 1) {  // single cell along this axis: periodic self-neighbour
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          nb_lo[v] = a_hi[v];
-          nb_hi[v] = a_lo[v];
-        }
-      } else {
-        const int ly = (axis == 1) ? lo_c : cy, lz = (axis == 2) ? lo_c : cz;
-        const int hy = (axis == 1) ? hi_c : cy, hz = (axis == 2) ? hi_c : cz;
-        const size_t lbase = ((size_t)cx + (size_t)C0 * ((size_t)ly + (size_t)C1 * lz)) * NV * NPE;
-        const size_t hbase = ((size_t)cx + (size_t)C0 * ((size_t)hy + (size_t)C1 * hz)) * NV * NPE;
-        const int n_lo = G::node(axis, tr, N - 1), n_hi = G::node(axis, tr, 0);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          nb_lo[v] = stage_input<EXACT>(p, lbase + (size_t)v * NPE + n_lo);
-          nb_hi[v] = stage_input<EXACT>(p, hbase + (size_t)v * NPE + n_hi);
-        }
+        nb_lo[v] = ea > 0 ? trc(axis, el - step_el, 1, v, tr) : halo(axis, 0, fidx, v, tr);
+        nb_hi[v] = ea < va - 1 ? trc(axis, el + step_el, 0, v, tr) : halo(axis, 1, fidx, v, tr);
       }
       double fo[NV], so, fn[NV], sn, fhat[NV];
       const double lift = p.lift[axis];
@@ -480,7 +592,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 #pragma unroll
         for (int v = 0; v < NV; ++v)
 #pragma unroll
-          for (int k = 0; k < N; ++k) fld(sP, el, v, G::node(axis, tr, k)) = D[v][k];
+          for (int k = 0; k < N; ++k) fld(sU, el, v, G::node(axis, tr, k)) = D[v][k];
       }
     }
   }
@@ -503,8 +615,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         bool finite = true;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          const double s = (DIM > 1) ? fld(sS, el, v, n) : S[v][k];
-          un[v] = A::mac(s, p.b_last, kv[v]);  // u += b_i k_i (solver.hpp:69-75)
+          un[v] = A::mac(fld(sS, el, v, n), p.b_last, kv[v]);  // u += b_i k_i (solver.hpp:69-75)
           p.out[ebase + (size_t)v * NPE + n] = un[v];
           finite = finite && isfinite(un[v]);
         }
@@ -524,15 +635,15 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     }
   }
   if (KIND == 1 && p.is_last && p.scan_alpha) {
-    alpha = warp_max(alpha);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) sR[warp] = alpha;
+    // block max of the non-negative wavespeeds on their IEEE bit patterns
+    // (valid for partial warps), then one global atomic per CTA
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(sR);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double a = 0.0;
-      for (int w = 0; w < (G::THREADS + 31) / 32; ++w) a = dmax(a, sR[w]);
-      atomicMax(&ctl->alpha_bits, (unsigned long long)__double_as_longlong(a));
-    }
+    if (threadIdx.x == 0) red[0] = 0ull;
+    __syncthreads();
+    atomicMax(red, (unsigned long long)__double_as_longlong(alpha));
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&ctl->alpha_bits, red[0]);
   }
 }
 

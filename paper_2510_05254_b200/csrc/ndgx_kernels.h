@@ -12,7 +12,7 @@ using StageFn = void (*)(const StageArgs);
 struct StageKernel {
   StageFn fn = nullptr;
   int threads = 0;
-  int te = 0;           // elements (x-cells) per CTA tile
+  int tile[3] = {1, 1, 1};  // elements per CTA tile along x, y, z
   int smem_base = 0;    // dynamic shared memory, non-last stages
   int smem_last = 0;    // dynamic shared memory, last stage
 };
@@ -26,7 +26,9 @@ StageKernel make_stage_kernel() {
   StageKernel k;
   k.fn = &stage_kernel<DIM, N, KIND, EXACT>;
   k.threads = G::THREADS;
-  k.te = G::TE;
+  k.tile[0] = G::TX;
+  k.tile[1] = G::TY;
+  k.tile[2] = G::TZ;
   k.smem_base = G::SMEM_BASE;
   k.smem_last = G::SMEM_LAST;
   return k;

@@ -106,22 +106,22 @@ struct ndgx_solver {
     StageArgs s;
     std::memset(&s, 0, sizeof(s));
     s.u = u_buf(par);
-    s.na = 0;
-    for (int j = 0; j < i; ++j) {
-      if (a[i][j] == 0.0) continue;  // solver.hpp:58
-      s.ka[s.na] = k_buf(j, par);
-      s.ca[s.na] = a[i][j];
-      ++s.na;
-    }
     s.is_last = (!rhs_only && i == stages - 1) ? 1 : 0;
-    s.nb = 0;
+    // union (ascending j) of the K_j read by the stage input (a_ij != 0,
+    // solver.hpp:58) and, at the last stage, by S (b_j != 0, solver.hpp:71)
+    s.nu = 0;
+    for (int j = 0; j < i; ++j) {
+      const bool ua = a[i][j] != 0.0;
+      const bool ub = s.is_last && b[j] != 0.0;
+      if (!ua && !ub) continue;
+      s.ku[s.nu] = k_buf(j, par);
+      s.ca[s.nu] = a[i][j];
+      s.cb[s.nu] = b[j];
+      if (ua) s.amask |= 1 << s.nu;
+      if (ub) s.bmask |= 1 << s.nu;
+      ++s.nu;
+    }
     if (s.is_last) {
-      for (int j = 0; j < i; ++j) {
-        if (b[j] == 0.0) continue;  // solver.hpp:71
-        s.kb[s.nb] = k_buf(j, par);
-        s.cb[s.nb] = b[j];
-        ++s.nb;
-      }
       s.b_last = b[i];
       s.out = out_buf(par);
     } else {
@@ -144,8 +144,9 @@ struct ndgx_solver {
   }
 
   void launch_stage(const StageArgs& s) const {
-    const int ntx = (cells[0] + kern.te - 1) / kern.te;
-    const long long grid = (long long)ntx * cells[1] * cells[2];
+    const long long grid = (long long)((cells[0] + kern.tile[0] - 1) / kern.tile[0]) *
+                           ((cells[1] + kern.tile[1] - 1) / kern.tile[1]) *
+                           ((cells[2] + kern.tile[2] - 1) / kern.tile[2]);
     const int smem = s.is_last ? kern.smem_last : kern.smem_base;
     kern.fn<<<(unsigned)grid, kern.threads, smem, stream>>>(s);
   }
