@@ -152,11 +152,15 @@ struct Geo {
   static constexpr int OFF_U = 0;                           // U_s, later the partial dudt P
   static constexpr int OFF_F = OFF_U + ARR;                 // F_axis for axes 1..DIM-1
   static constexpr int OFF_T = OFF_F + (DIM - 1) * ARR;     // own U traces, axes 1..DIM-1
-  static constexpr int OFF_H = OFF_T + (DIM - 1) * TE * 2 * NV * L;  // out-of-tile halo U_s
+  static constexpr int OFF_H = OFF_T + (DIM - 1) * TE * 2 * (NV + 1) * L;  // halo U_s
   static constexpr int OFF_R = OFF_H + HSIZE;               // reduction scratch
   static constexpr int OFF_S = OFF_R + 32;                  // S (last stage)
   static constexpr int SMEM_BASE = OFF_S * 8;
   static constexpr int SMEM_LAST = (OFF_S + ARR) * 8;
+  // CTAs per SM allowed by shared memory (228 KB/SM, 1 KB reserved per CTA);
+  // registers are capped so they never become the tighter limit
+  static constexpr int CTAS_SMEM = 232448 / (SMEM_BASE + 1024);
+  static constexpr int MINB = CTAS_SMEM < 1 ? 1 : (CTAS_SMEM > 8 ? 8 : CTAS_SMEM);
 
   // node index of position k along `axis` for transverse line index tr
   static __device__ __forceinline__ int node(int axis, int tr, int k) {
@@ -259,131 +263,129 @@ struct TileCtx {
 // Node-parallel, coalesced, all terms in flight: U_s = u + sum a_sj K_j and
 // (last stage) S = u + sum b_j K_j for every node of the tile, into padded
 // shared memory; then the out-of-tile neighbours' face planes into the halo.
+// One warp per element (its NV*NPE doubles are contiguous in HBM), lanes
+// over PAIR-sized chunks, compile-time trip counts: no per-item div/mod.
 template <int DIM, int N, int KIND, bool EXACT, int NU>
 __device__ __forceinline__ void prepass(const StageArgs& p, const TileCtx& tc, double* smem) {
   using G = Geo<DIM, N, KIND>;
   using A = Ar<EXACT>;
-  constexpr int NV = G::NV, NPE = G::NPE, LP = G::LP, TE = G::TE, PAIR = G::PAIR;
-  constexpr int PER_EL = NV * NPE / PAIR;  // items per element
-  constexpr int ITEMS = TE * PER_EL;
-  // ~8 double2 loads in flight per thread whatever the number of terms
-  constexpr int UNR = (8 / (1 + NU)) < 1 ? 1 : ((8 / (1 + NU)) > 4 ? 4 : 8 / (1 + NU));
-  const int T = blockDim.x;
+  constexpr int NV = G::NV, NPE = G::NPE, LP = G::LP, TE = G::TE, PAIR = G::PAIR, L = G::L;
+  constexpr int CH = NV * NPE / PAIR;      // chunks per element
+  constexpr int CNT = (CH + 31) / 32;      // chunks per lane
+  constexpr int CB0 = 8 / (1 + NU) < 1 ? 1 : 8 / (1 + NU);
+  constexpr int CB = CB0 < CNT ? CB0 : CNT;  // chunks per load batch
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
   const int C0 = p.cells[0], C1 = p.cells[1];
   double* sU = smem + G::OFF_U;
   double* sS = smem + G::OFF_S;
   const bool last = p.is_last;
 
-  for (int base = threadIdx.x; base < ITEMS; base += UNR * T) {
-    Vec<PAIR> uu[UNR], kk[UNR][NU > 0 ? NU : 1];
-    size_t gaddr[UNR];
-    int saddr[UNR];
-    bool ok[UNR];
+  for (int el = warp; el < TE; el += nwarps) {
+    const int ex = el % G::TX, ey = (el / G::TX) % G::TY, ez = el / (G::TX * G::TY);
+    if (!(ex < tc.vx && ey < tc.vy && ez < tc.vz)) continue;
+    const size_t e = (size_t)(tc.x0 + ex) + (size_t)C0 * ((size_t)(tc.y0 + ey) + (size_t)C1 * (tc.z0 + ez));
+    const size_t gb = e * NV * NPE;
+    // batches of CB chunks per lane keep ~8 double2 loads in flight
 #pragma unroll
-    for (int w = 0; w < UNR; ++w) {
-      const int q = base + w * T;
-      const int el = q / PER_EL;
-      const int r = (q - el * PER_EL) * PAIR;
-      const int ex = el % G::TX, ey = (el / G::TX) % G::TY, ez = el / (G::TX * G::TY);
-      ok[w] = q < ITEMS && ex < tc.vx && ey < tc.vy && ez < tc.vz;
-      const size_t e = (size_t)(tc.x0 + ex) + (size_t)C0 * ((size_t)(tc.y0 + ey) + (size_t)C1 * (tc.z0 + ez));
-      gaddr[w] = e * NV * NPE + r;
-      const int v = r / NPE, n = r - v * NPE;
-      saddr[w] = (el * NV + v) * LP + G::sn(n);
-      if (ok[w]) {
-        uu[w] = Vec<PAIR>::ld(p.u + gaddr[w]);
+    for (int c0 = 0; c0 < CNT; c0 += CB) {
+      Vec<PAIR> uu[CB], kk[CB][NU > 0 ? NU : 1];
 #pragma unroll
-        for (int t = 0; t < NU; ++t) kk[w][t] = Vec<PAIR>::ld(p.ku[t] + gaddr[w]);
+      for (int cb = 0; cb < CB; ++cb) {
+        const int c = c0 + cb;
+        const int r = (lane + 32 * c) * PAIR;
+        if (c < CNT && (CH % 32 == 0 || lane + 32 * c < CH)) {
+          uu[cb] = Vec<PAIR>::ld(p.u + gb + r);
+#pragma unroll
+          for (int t = 0; t < NU; ++t) kk[cb][t] = Vec<PAIR>::ld(p.ku[t] + gb + r);
+        }
       }
-    }
 #pragma unroll
-    for (int w = 0; w < UNR; ++w) {
-      if (!ok[w]) continue;
-      double U0 = uu[w].x, S0 = uu[w].x;
-#pragma unroll
-      for (int t = 0; t < NU; ++t) {
-        if (p.amask >> t & 1) U0 = A::mac(U0, p.ca[t], kk[w][t].x);
-        if (last && (p.bmask >> t & 1)) S0 = A::mac(S0, p.cb[t], kk[w][t].x);
-      }
-      sU[saddr[w]] = U0;
-      if (last) sS[saddr[w]] = S0;
-      if constexpr (PAIR == 2) {
-        double U1 = uu[w].y, S1 = uu[w].y;
+      for (int cb = 0; cb < CB; ++cb) {
+        const int c = c0 + cb;
+        const int r = (lane + 32 * c) * PAIR;
+        if (!(c < CNT && (CH % 32 == 0 || lane + 32 * c < CH))) continue;
+        const int v = r / NPE, n = r - v * NPE;
+        const int sa = (el * NV + v) * LP + G::sn(n);
+        double U0 = uu[cb].x, S0 = uu[cb].x;
 #pragma unroll
         for (int t = 0; t < NU; ++t) {
-          if (p.amask >> t & 1) U1 = A::mac(U1, p.ca[t], kk[w][t].y);
-          if (last && (p.bmask >> t & 1)) S1 = A::mac(S1, p.cb[t], kk[w][t].y);
+          if (p.amask >> t & 1) U0 = A::mac(U0, p.ca[t], kk[cb][t].x);
+          if (last && (p.bmask >> t & 1)) S0 = A::mac(S0, p.cb[t], kk[cb][t].x);
         }
-        sU[saddr[w] + 1] = U1;  // n and n+1 share an x-line (N even)
-        if (last) sS[saddr[w] + 1] = S1;
+        sU[sa] = U0;
+        if (last) sS[sa] = S0;
+        if constexpr (PAIR == 2) {
+          double U1 = uu[cb].y, S1 = uu[cb].y;
+#pragma unroll
+          for (int t = 0; t < NU; ++t) {
+            if (p.amask >> t & 1) U1 = A::mac(U1, p.ca[t], kk[cb][t].y);
+            if (last && (p.bmask >> t & 1)) S1 = A::mac(S1, p.cb[t], kk[cb][t].y);
+          }
+          sU[sa + 1] = U1;  // n and n+1 share an x-line (N even)
+          if (last) sS[sa + 1] = S1;
+        }
       }
     }
   }
 
-  // halo: the face plane of each out-of-tile neighbour (always loaded, also
-  // when the periodic wrap lands inside the tile -- the values are identical)
-  constexpr int L = G::L;
-  constexpr int H0 = 2 * G::HF0 * NV * L;
-  constexpr int H1 = DIM > 1 ? 2 * G::HF1 * NV * L : 0;
-  constexpr int H2 = DIM > 2 ? 2 * G::HF2 * NV * L : 0;
-  constexpr int HITEMS = H0 + H1 + H2;
+  // halo: the face plane of each out-of-tile neighbour, one warp per face
+  // (always loaded, also when the periodic wrap lands inside the tile --
+  // the values are identical)
+  constexpr int HV = NV * L;              // values per face plane
+  constexpr int HC = (HV + 31) / 32;
+  constexpr int NF0 = 2 * G::HF0, NF1 = DIM > 1 ? 2 * G::HF1 : 0, NF2 = DIM > 2 ? 2 * G::HF2 : 0;
   double* sH = smem + G::OFF_H;
-  for (int base = threadIdx.x; base < HITEMS; base += 2 * T) {
-    double hu[2], hk[2][NU > 0 ? NU : 1];
-    int hdst[2];
-    bool ok[2];
+  for (int fq = warp; fq < NF0 + NF1 + NF2; fq += nwarps) {
+    int axis, f2;
+    if (fq < NF0) { axis = 0; f2 = fq; }
+    else if (fq < NF0 + NF1) { axis = 1; f2 = fq - NF0; }
+    else { axis = 2; f2 = fq - NF0 - NF1; }
+    const int nf = axis == 0 ? G::HF0 : (axis == 1 ? G::HF1 : G::HF2);
+    const int side = f2 / nf, f = f2 - side * nf;
+    int ex, ey, ez;
+    if (axis == 0) { ey = f % G::TY; ez = f / G::TY; ex = side ? tc.vx - 1 : 0; }
+    else if (axis == 1) { ex = f % G::TX; ez = f / G::TX; ey = side ? tc.vy - 1 : 0; }
+    else { ex = f % G::TX; ey = f / G::TX; ez = side ? tc.vz - 1 : 0; }
+    if (!(ex < tc.vx && ey < tc.vy && ez < tc.vz)) continue;
+    int c[3] = {tc.x0 + ex, tc.y0 + ey, tc.z0 + ez};
+    const int cn = p.cells[axis];
+    c[axis] = side ? (c[axis] + 1 == cn ? 0 : c[axis] + 1) : (c[axis] == 0 ? cn - 1 : c[axis] - 1);
+    const size_t gb = ((size_t)c[0] + (size_t)C0 * ((size_t)c[1] + (size_t)C1 * c[2])) * NV * NPE;
+    double* dst = sH + G::halo_off(axis) + (side * nf + f) * HV;
+    double hu[HC], hk[HC][NU > 0 ? NU : 1];
 #pragma unroll
-    for (int w = 0; w < 2; ++w) {
-      const int q = base + w * T;
-      ok[w] = q < HITEMS;
-      int axis, r;
-      if (q < H0) { axis = 0; r = q; }
-      else if (q < H0 + H1) { axis = 1; r = q - H0; }
-      else { axis = 2; r = q - H0 - H1; }
-      const int nf = axis == 0 ? G::HF0 : (axis == 1 ? G::HF1 : G::HF2);
-      // r = ((side * nf + f) * NV + v) * L + t
-      const int t = r % L;
-      const int v = (r / L) % NV;
-      const int f = (r / (L * NV)) % nf;
-      const int side = r / (L * NV * nf);
-      // tile element on the tile boundary: transverse coords from f
-      int ex, ey, ez;
-      if (axis == 0) { ey = f % G::TY; ez = f / G::TY; ex = side ? tc.vx - 1 : 0; }
-      else if (axis == 1) { ex = f % G::TX; ez = f / G::TX; ey = side ? tc.vy - 1 : 0; }
-      else { ex = f % G::TX; ey = f / G::TX; ez = side ? tc.vz - 1 : 0; }
-      ok[w] = ok[w] && ex < tc.vx && ey < tc.vy && ez < tc.vz;
-      int c[3] = {tc.x0 + ex, tc.y0 + ey, tc.z0 + ez};
-      const int cn = p.cells[axis];
-      c[axis] = side ? (c[axis] + 1 == cn ? 0 : c[axis] + 1) : (c[axis] == 0 ? cn - 1 : c[axis] - 1);
-      const size_t e = (size_t)c[0] + (size_t)C0 * ((size_t)c[1] + (size_t)C1 * c[2]);
-      const int n = G::node(axis, t, side ? 0 : N - 1);
-      const size_t g = e * NV * NPE + (size_t)v * NPE + n;
-      hdst[w] = q - (axis == 0 ? 0 : (axis == 1 ? H0 : H0 + H1)) + G::halo_off(axis);
-      if (ok[w]) {
-        hu[w] = __ldg(p.u + g);
+    for (int cc = 0; cc < HC; ++cc) {
+      const int q = lane + 32 * cc;  // q = v * L + t
+      if (HV % 32 == 0 || q < HV) {
+        const int v = q / L, t = q - v * L;
+        const size_t g = gb + (size_t)v * NPE + G::node(axis, t, side ? 0 : N - 1);
+        hu[cc] = __ldg(p.u + g);
 #pragma unroll
-        for (int tt = 0; tt < NU; ++tt) hk[w][tt] = __ldg(p.ku[tt] + g);
+        for (int tt = 0; tt < NU; ++tt) hk[cc][tt] = __ldg(p.ku[tt] + g);
       }
     }
 #pragma unroll
-    for (int w = 0; w < 2; ++w) {
-      if (!ok[w]) continue;
-      double U0 = hu[w];
+    for (int cc = 0; cc < HC; ++cc) {
+      const int q = lane + 32 * cc;
+      if (!(HV % 32 == 0 || q < HV)) continue;
+      double U0 = hu[cc];
 #pragma unroll
       for (int tt = 0; tt < NU; ++tt)
-        if (p.amask >> tt & 1) U0 = A::mac(U0, p.ca[tt], hk[w][tt]);
-      sH[hdst[w]] = U0;
+        if (p.amask >> tt & 1) U0 = A::mac(U0, p.ca[tt], hk[cc][tt]);
+      dst[q] = U0;
     }
   }
 }
 
 // ============================================================ stage kernel
 template <int DIM, int N, int KIND, bool EXACT>
-__global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS)
+__global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS, Geo<DIM, N, KIND>::MINB)
 stage_kernel(const __grid_constant__ StageArgs p) {
   using G = Geo<DIM, N, KIND>;
   using A = Ar<EXACT>;
   constexpr int NV = G::NV, L = G::L, NPE = G::NPE, LP = G::LP, TE = G::TE;
+  constexpr int NT = NV + 1;  // trace slots per face node: U (NV) + one-sided wavespeed
   extern __shared__ double smem[];
 
   Control* ctl = p.ctl;
@@ -406,28 +408,40 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 
   const int tid = threadIdx.x;
   const int el = tid / L;
-  const int tr = tid % L;  // transverse line index (same count for every axis)
+  const int tr = tid - el * L;  // transverse line index (same count for every axis)
   const int ex = el % G::TX, ey = (el / G::TX) % G::TY, ez = el / (G::TX * G::TY);
   const bool valid = ex < tc.vx && ey < tc.vy && ez < tc.vz;
   const int cx = tc.x0 + ex, cy = tc.y0 + ey, cz = tc.z0 + ez;
   const size_t e = (size_t)cx + (size_t)C0 * ((size_t)cy + (size_t)C1 * cz);
   const size_t ebase = e * NV * NPE;
+  const int tj = DIM > 1 ? tr % N : 0, tk = DIM > 2 ? tr / N : 0;  // x-line's (j, k)
 
   const double dt = p.rhs_only ? 1.0 : ctl->dt;
   const long long step = p.rhs_only ? 0 : ctl->steps;
 
   double* sU = smem + G::OFF_U;  // [TE][NV][LP]  U_s, then P
   double* sF = smem + G::OFF_F;  // [DIM-1][TE][NV][LP]
-  double* sT = smem + G::OFF_T;  // [DIM-1][TE][2][NV][L]
+  double* sT = smem + G::OFF_T;  // [DIM-1][TE][2][NT][L]
   double* sH = smem + G::OFF_H;  // halo
   double* sR = smem + G::OFF_R;  // [32]
   double* sS = smem + G::OFF_S;  // [TE][NV][LP] (last stage)
 
-  auto fld = [&](double* base, int elx, int v, int n) -> double& {
-    return base[(elx * NV + v) * LP + G::sn(n)];
+  // padded shared slot of the node at position k along `axis` of line tr:
+  // sbase(axis) + k * sstride(axis)
+  auto sbase = [&](int axis) -> int {
+    if (axis == 0) return tr * (N + 1);
+    if (axis == 1) return tj /*= i0*/ + (N + 1) * N * tk;
+    return tj + (N + 1) * tk;  // axis 2: tr = i0 + N*i1
   };
+  auto sstride = [](int axis) -> int { return axis == 0 ? 1 : (axis == 1 ? N + 1 : (N + 1) * N); };
+  auto gbase = [&](int axis) -> int {  // node index of k = 0
+    if (axis == 0) return tr * N;
+    if (axis == 1) return tj + N * N * tk;
+    return tr;
+  };
+  auto gstride = [](int axis) -> int { return axis == 0 ? 1 : (axis == 1 ? N : N * N); };
   auto trc = [&](int axis, int elx, int side, int v, int t) -> double& {  // axis >= 1
-    return sT[((((axis - 1) * TE + elx) * 2 + side) * NV + v) * L + t];
+    return sT[((((axis - 1) * TE + elx) * 2 + side) * NT + v) * L + t];
   };
   auto halo = [&](int axis, int side, int f, int v, int t) -> double {
     return sH[G::halo_off(axis) + ((side * G::halo_faces(axis) + f) * NV + v) * L + t];
@@ -451,22 +465,24 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 
   // ---------------------------------------------------------------- phase X
   double D[NV][N];
+  const int xl = el * NV * LP + sbase(0);  // this x-line in sU / sF / sS
   if (valid) {
     double U[NV][N];
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int i = 0; i < N; ++i) U[v][i] = fld(sU, el, v, i + N * tr);
+      for (int i = 0; i < N; ++i) U[v][i] = sU[xl + v * LP + i];
     // fluxes at every node of the line, every axis
     double FX[NV][N];
     double s_lo = 0.0, s_hi = 0.0;
+    const bool yb = DIM > 1 && (tj == 0 || tj == N - 1);
+    const bool zb = DIM > 2 && (tk == 0 || tk == N - 1);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double un[NV], f[NV], sp;
       if (KIND == 1 && !(U[0][i] > 0.0)) {
         // first bad node of the reference's x-volume traversal: (cell, (j,k), i)
-        const int j = (DIM > 1) ? tr % N : 0, k = (DIM > 2) ? tr / N : 0;
-        const int nkey = (DIM == 1) ? i : (DIM == 2 ? j * N + i : (j * N + k) * N + i);
+        const int nkey = (DIM == 1) ? i : (DIM == 2 ? tj * N + i : (tj * N + tk) * N + i);
         record_error(ctl, error_key(step, p.phase, aos_cell(cx, cy, cz), nkey));
       }
 #pragma unroll
@@ -480,12 +496,47 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       for (int d = 1; d < DIM; ++d) {
         flux<DIM, KIND, EXACT>(p, un, d, f, sp);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) fld(sF + (d - 1) * G::ARR, el, v, i + N * tr) = f[v];
+        for (int v = 0; v < NV; ++v) sF[(d - 1) * G::ARR + xl + v * LP + i] = f[v];
+        // own face traces (state + one-sided speed) for the y/z phases
+        if (d == 1 && yb) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) trc(1, el, tj == 0 ? 0 : 1, v, i + N * tk) = un[v];
+          trc(1, el, tj == 0 ? 0 : 1, NV, i + N * tk) = sp;
+        }
+        if (d == 2 && zb) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) trc(2, el, tk == 0 ? 0 : 1, v, i + N * tj) = un[v];
+          trc(2, el, tk == 0 ? 0 : 1, NV, i + N * tj) = sp;
+        }
       }
     }
-    // volume x: out(=0) += sum_l K[k][l] F_l   (solver.cpp:246-256)
+    // x faces (solver.cpp:268-306): face at i=0 (we are its + side) and at
+    // i=N-1 (we are its - side); the minus state is always the lower cell.
+    // The fluxes are formed first so U can retire before the volume term.
+    double fh_lo[NV], fh_hi[NV];
+    {
+      double nb_lo[NV], nb_hi[NV];
+      const int fx = ey + G::TY * ez;
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
+      for (int v = 0; v < NV; ++v) {
+        nb_lo[v] = ex > 0 ? sU[xl - NV * LP + v * LP + (N - 1)] : halo(0, 0, fx, v, tr);
+        nb_hi[v] = ex < tc.vx - 1 ? sU[xl + NV * LP + v * LP] : halo(0, 1, fx, v, tr);
+      }
+      double fo[NV], fn[NV], sn, uo[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) { fo[v] = FX[v][0]; uo[v] = U[v][0]; }
+      flux<DIM, KIND, EXACT>(p, nb_lo, 0, fn, sn);
+      lax_friedrichs<NV, EXACT>(nb_lo, uo, fn, fo, sn, s_lo, fh_lo);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) { fo[v] = FX[v][N - 1]; uo[v] = U[v][N - 1]; }
+      flux<DIM, KIND, EXACT>(p, nb_hi, 0, fn, sn);
+      lax_friedrichs<NV, EXACT>(uo, nb_hi, fo, fn, s_hi, sn, fh_hi);
+    }
+    // volume x: out(=0) += sum_l K[k][l] F_l (solver.cpp:246-256), then the
+    // lifted face fluxes: out += lift F^ at i=0, out -= lift F^ at i=N-1
+    const double lift = p.lift[0];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double acc = 0.0;
@@ -493,45 +544,9 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         for (int l = 0; l < N; ++l) acc = A::mac(acc, p.K[0][k * N + l], FX[v][l]);
         D[v][k] = zero_plus(acc);
       }
-    // own y/z face traces for the later phases (sU becomes P below)
-    if (DIM > 1) {
-      const int j = tr % N, k = tr / N;
-      if (j == 0 || j == N - 1) {
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) trc(1, el, j == 0 ? 0 : 1, v, i + N * k) = U[v][i];
-      }
-      if (DIM > 2 && (k == 0 || k == N - 1)) {
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) trc(2, el, k == 0 ? 0 : 1, v, i + N * j) = U[v][i];
-      }
+      D[v][0] = A::add(D[v][0], A::mul(lift, fh_lo[v]));
+      D[v][N - 1] = A::sub(D[v][N - 1], A::mul(lift, fh_hi[v]));
     }
-    // x faces (solver.cpp:268-306): face at i=0 (we are its + side) and at
-    // i=N-1 (we are its - side); the minus state is always the lower cell
-    double nb_lo[NV], nb_hi[NV];
-    const int fx = ey + G::TY * ez;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      nb_lo[v] = ex > 0 ? fld(sU, el - 1, v, (N - 1) + N * tr) : halo(0, 0, fx, v, tr);
-      nb_hi[v] = ex < tc.vx - 1 ? fld(sU, el + 1, v, N * tr) : halo(0, 1, fx, v, tr);
-    }
-    double fo[NV], fn[NV], sn, fhat[NV], uo[NV];
-    const double lift = p.lift[0];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) { fo[v] = FX[v][0]; uo[v] = U[v][0]; }
-    flux<DIM, KIND, EXACT>(p, nb_lo, 0, fn, sn);
-    lax_friedrichs<NV, EXACT>(nb_lo, uo, fn, fo, sn, s_lo, fhat);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) D[v][0] = A::add(D[v][0], A::mul(lift, fhat[v]));
-#pragma unroll
-    for (int v = 0; v < NV; ++v) { fo[v] = FX[v][N - 1]; uo[v] = U[v][N - 1]; }
-    flux<DIM, KIND, EXACT>(p, nb_hi, 0, fn, sn);
-    lax_friedrichs<NV, EXACT>(uo, nb_hi, fo, fn, s_hi, sn, fhat);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) D[v][N - 1] = A::sub(D[v][N - 1], A::mul(lift, fhat[v]));
   }
   if (DIM > 1) {
     __syncthreads();  // every x-face read of sU is done: sU becomes P
@@ -539,7 +554,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 #pragma unroll
       for (int v = 0; v < NV; ++v)
 #pragma unroll
-        for (int i = 0; i < N; ++i) fld(sU, el, v, i + N * tr) = D[v][i];
+        for (int i = 0; i < N; ++i) sU[xl + v * LP + i] = D[v][i];
     }
   }
 
@@ -548,51 +563,57 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   for (int axis = 1; axis < DIM; ++axis) {
     __syncthreads();
     if (valid) {
-      double F[NV][N];
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int k = 0; k < N; ++k) F[v][k] = fld(sF + (axis - 1) * G::ARR, el, v, G::node(axis, tr, k));
-      // volume: partial + sum_l K[k][l] F_l
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double acc = 0.0;
-#pragma unroll
-          for (int l = 0; l < N; ++l) acc = A::mac(acc, p.K[axis][k * N + l], F[v][l]);
-          D[v][k] = A::add(fld(sU, el, v, G::node(axis, tr, k)), acc);
-        }
-      // faces along this axis: own traces, neighbours from the tile or the halo
+      const int ab = el * NV * LP + sbase(axis);
+      const int as = sstride(axis);
+      const double* Fa = sF + (axis - 1) * G::ARR + ab;
+      // faces along this axis first (own traces; neighbours from the tile or
+      // the halo), so that only one variable's flux line is live at a time
       const int ea = axis == 1 ? ey : ez;
       const int va = axis == 1 ? tc.vy : tc.vz;
       const int step_el = axis == 1 ? G::TX : G::TX * G::TY;
       const int fidx = axis == 1 ? ex + G::TX * ez : ex + G::TX * ey;
-      double a_lo[NV], a_hi[NV], nb_lo[NV], nb_hi[NV];
+      double fh_lo[NV], fh_hi[NV];
+      {
+        double a_lo[NV], a_hi[NV], nb_lo[NV], nb_hi[NV], fo[NV], fn[NV], sn;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          a_lo[v] = trc(axis, el, 0, v, tr);
+          a_hi[v] = trc(axis, el, 1, v, tr);
+          nb_lo[v] = ea > 0 ? trc(axis, el - step_el, 1, v, tr) : halo(axis, 0, fidx, v, tr);
+          nb_hi[v] = ea < va - 1 ? trc(axis, el + step_el, 0, v, tr) : halo(axis, 1, fidx, v, tr);
+        }
+        const double so_lo = trc(axis, el, 0, NV, tr), so_hi = trc(axis, el, 1, NV, tr);
+        flux<DIM, KIND, EXACT>(p, nb_lo, axis, fn, sn);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) fo[v] = Fa[v * LP];
+        lax_friedrichs<NV, EXACT>(nb_lo, a_lo, fn, fo, sn, so_lo, fh_lo);
+        flux<DIM, KIND, EXACT>(p, nb_hi, axis, fn, sn);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) fo[v] = Fa[v * LP + (N - 1) * as];
+        lax_friedrichs<NV, EXACT>(a_hi, nb_hi, fo, fn, so_hi, sn, fh_hi);
+      }
+      // volume: partial + sum_l K[k][l] F_l, then the lifted face fluxes
+      const double lift = p.lift[axis];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        a_lo[v] = trc(axis, el, 0, v, tr);
-        a_hi[v] = trc(axis, el, 1, v, tr);
-        nb_lo[v] = ea > 0 ? trc(axis, el - step_el, 1, v, tr) : halo(axis, 0, fidx, v, tr);
-        nb_hi[v] = ea < va - 1 ? trc(axis, el + step_el, 0, v, tr) : halo(axis, 1, fidx, v, tr);
+        double F[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) F[k] = Fa[v * LP + k * as];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < N; ++l) acc = A::mac(acc, p.K[axis][k * N + l], F[l]);
+          D[v][k] = A::add(sU[ab + v * LP + k * as], acc);
+        }
+        D[v][0] = A::add(D[v][0], A::mul(lift, fh_lo[v]));
+        D[v][N - 1] = A::sub(D[v][N - 1], A::mul(lift, fh_hi[v]));
       }
-      double fo[NV], so, fn[NV], sn, fhat[NV];
-      const double lift = p.lift[axis];
-      flux<DIM, KIND, EXACT>(p, nb_lo, axis, fn, sn);
-      flux<DIM, KIND, EXACT>(p, a_lo, axis, fo, so);
-      lax_friedrichs<NV, EXACT>(nb_lo, a_lo, fn, fo, sn, so, fhat);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) D[v][0] = A::add(D[v][0], A::mul(lift, fhat[v]));
-      flux<DIM, KIND, EXACT>(p, nb_hi, axis, fn, sn);
-      flux<DIM, KIND, EXACT>(p, a_hi, axis, fo, so);
-      lax_friedrichs<NV, EXACT>(a_hi, nb_hi, fo, fn, so, sn, fhat);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) D[v][N - 1] = A::sub(D[v][N - 1], A::mul(lift, fhat[v]));
       if (axis < DIM - 1) {
 #pragma unroll
         for (int v = 0; v < NV; ++v)
 #pragma unroll
-          for (int k = 0; k < N; ++k) fld(sU, el, v, G::node(axis, tr, k)) = D[v][k];
+          for (int k = 0; k < N; ++k) sU[ab + v * LP + k * as] = D[v][k];
       }
     }
   }
@@ -601,29 +622,33 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   constexpr int FA = DIM - 1;  // axis of the final owner
   double alpha = 0.0;
   if (valid) {
+    const int sb = el * NV * LP + sbase(FA);
+    const int ss = sstride(FA);
+    double* gout = p.out + ebase + gbase(FA);
+    const int gs = gstride(FA);
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      const int n = G::node(FA, tr, k);
       double kv[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) kv[v] = A::mul(D[v][k], dt);  // k_i *= dt (solver.hpp:66-67)
       if (!p.is_last) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) p.out[ebase + (size_t)v * NPE + n] = kv[v];
+        for (int v = 0; v < NV; ++v) gout[v * NPE + k * gs] = kv[v];
       } else {
         double un[NV];
         bool finite = true;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          un[v] = A::mac(fld(sS, el, v, n), p.b_last, kv[v]);  // u += b_i k_i (solver.hpp:69-75)
-          p.out[ebase + (size_t)v * NPE + n] = un[v];
+          un[v] = A::mac(sS[sb + v * LP + k * ss], p.b_last, kv[v]);  // u += b_i k_i (solver.hpp:69-75)
+          gout[v * NPE + k * gs] = un[v];
           finite = finite && isfinite(un[v]);
         }
         if (!finite) record_error(ctl, error_key(step, kPhaseInstability, 0, 0));
         if (KIND == 1 && p.scan_alpha) {
           // the next step's max_wavespeed_bound (solver.cpp:323-332), fused
           if (!(un[0] > 0.0)) {
-            record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(cx, cy, cz), G::aos_node(n)));
+            record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(cx, cy, cz),
+                                        G::aos_node(gbase(FA) + k * gs)));
           } else {
             double m = 0.0;
 #pragma unroll
