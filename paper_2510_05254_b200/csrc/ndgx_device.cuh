@@ -154,9 +154,8 @@ struct Geo {
   static constexpr int OFF_T = OFF_F + (DIM - 1) * ARR;     // own U traces, axes 1..DIM-1
   static constexpr int OFF_H = OFF_T + (DIM - 1) * TE * 2 * (NV + 1) * L;  // halo U_s
   static constexpr int OFF_R = OFF_H + HSIZE;               // reduction scratch
-  static constexpr int OFF_S = OFF_R + 32;                  // S (last stage)
-  static constexpr int SMEM_BASE = OFF_S * 8;
-  static constexpr int SMEM_LAST = (OFF_S + ARR) * 8;
+  static constexpr int SMEM_BASE = (OFF_R + 32) * 8;
+  static constexpr int SMEM_LAST = SMEM_BASE;
   // CTAs per SM allowed by shared memory (228 KB/SM, 1 KB reserved per CTA);
   // registers are capped so they never become the tighter limit
   static constexpr int CTAS_SMEM = 232448 / (SMEM_BASE + 1024);
@@ -242,13 +241,14 @@ struct Vec;
 template <>
 struct Vec<1> {
   double x;
-  static __device__ __forceinline__ Vec ld(const double* p) { return Vec{__ldg(p)}; }
+  // coherent loads: at the last stage one term may alias the output slot
+  static __device__ __forceinline__ Vec ld(const double* p) { return Vec{*p}; }
 };
 template <>
 struct Vec<2> {
   double x, y;
   static __device__ __forceinline__ Vec ld(const double* p) {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 v = *reinterpret_cast<const double2*>(p);
     return Vec{v.x, v.y};
   }
 };
@@ -260,120 +260,136 @@ struct TileCtx {
 };
 
 // ------------------------------------------------------------ prepass
-// Node-parallel, coalesced, all terms in flight: U_s = u + sum a_sj K_j and
-// (last stage) S = u + sum b_j K_j for every node of the tile, into padded
-// shared memory; then the out-of-tile neighbours' face planes into the halo.
-// One warp per element (its NV*NPE doubles are contiguous in HBM), lanes
-// over PAIR-sized chunks, compile-time trip counts: no per-item div/mod.
+// Node-parallel, coalesced, all terms in flight: U_s = u + sum a_sj K_j for
+// every node of the tile into padded shared memory, and at the last stage
+// S = u + sum b_j K_j straight into the output array (read back by the
+// epilogue from L2; the slot is never read by other CTAs in that stage).
+// Then the out-of-tile neighbours' face planes into the halo.
+// Full warps only (THREADS need not be a multiple of 32); each warp takes
+// elements el = warp + NW*m (an element's NV*NPE doubles are contiguous in
+// HBM), lanes take PAIR-sized chunks, and (element, chunk) work is flattened
+// and batched so that ~8 double2 loads are in flight per lane.
 template <int DIM, int N, int KIND, bool EXACT, int NU>
 __device__ __forceinline__ void prepass(const StageArgs& p, const TileCtx& tc, double* smem) {
   using G = Geo<DIM, N, KIND>;
   using A = Ar<EXACT>;
   constexpr int NV = G::NV, NPE = G::NPE, LP = G::LP, TE = G::TE, PAIR = G::PAIR, L = G::L;
+  constexpr int NW = G::THREADS / 32;      // full warps (>= 2 for every instantiation)
   constexpr int CH = NV * NPE / PAIR;      // chunks per element
-  constexpr int CNT = (CH + 31) / 32;      // chunks per lane
+  constexpr int CNT = (CH + 31) / 32;      // chunks per lane per element
+  constexpr int EPW = (TE + NW - 1) / NW;  // elements per warp
+  constexpr int J = EPW * CNT;             // work items per lane
   constexpr int CB0 = 8 / (1 + NU) < 1 ? 1 : 8 / (1 + NU);
-  constexpr int CB = CB0 < CNT ? CB0 : CNT;  // chunks per load batch
+  constexpr int CB = CB0 < J ? CB0 : J;    // items per load batch
+  static_assert(NW >= 1, "stage kernel needs at least one full warp");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarps = (blockDim.x + 31) >> 5;
+  if (warp >= NW) return;  // the partial warp (if any) only joins the barriers
   const int C0 = p.cells[0], C1 = p.cells[1];
   double* sU = smem + G::OFF_U;
-  double* sS = smem + G::OFF_S;
   const bool last = p.is_last;
 
-  for (int el = warp; el < TE; el += nwarps) {
-    const int ex = el % G::TX, ey = (el / G::TX) % G::TY, ez = el / (G::TX * G::TY);
-    if (!(ex < tc.vx && ey < tc.vy && ez < tc.vz)) continue;
-    const size_t e = (size_t)(tc.x0 + ex) + (size_t)C0 * ((size_t)(tc.y0 + ey) + (size_t)C1 * (tc.z0 + ez));
-    const size_t gb = e * NV * NPE;
-    // batches of CB chunks per lane keep ~8 double2 loads in flight
 #pragma unroll
-    for (int c0 = 0; c0 < CNT; c0 += CB) {
-      Vec<PAIR> uu[CB], kk[CB][NU > 0 ? NU : 1];
+  for (int j0 = 0; j0 < J; j0 += CB) {
+    Vec<PAIR> uu[CB], kk[CB][NU > 0 ? NU : 1];
+    size_t ga[CB];
+    bool ok[CB];
 #pragma unroll
-      for (int cb = 0; cb < CB; ++cb) {
-        const int c = c0 + cb;
-        const int r = (lane + 32 * c) * PAIR;
-        if (c < CNT && (CH % 32 == 0 || lane + 32 * c < CH)) {
-          uu[cb] = Vec<PAIR>::ld(p.u + gb + r);
+    for (int b = 0; b < CB; ++b) {
+      const int j = j0 + b;
+      const int el = warp + NW * (j / CNT), c = j % CNT;
+      const int ex = el % G::TX, ey = (el / G::TX) % G::TY, ez = el / (G::TX * G::TY);
+      ok[b] = j < J && el < TE && ex < tc.vx && ey < tc.vy && ez < tc.vz &&
+              (CH % 32 == 0 || lane + 32 * c < CH);
+      const size_t e = (size_t)(tc.x0 + ex) + (size_t)C0 * ((size_t)(tc.y0 + ey) + (size_t)C1 * (tc.z0 + ez));
+      ga[b] = e * NV * NPE + (size_t)(lane + 32 * c) * PAIR;
+      if (ok[b]) {
+        uu[b] = Vec<PAIR>::ld(p.u + ga[b]);
 #pragma unroll
-          for (int t = 0; t < NU; ++t) kk[cb][t] = Vec<PAIR>::ld(p.ku[t] + gb + r);
-        }
+        for (int t = 0; t < NU; ++t) kk[b][t] = Vec<PAIR>::ld(p.ku[t] + ga[b]);
       }
+    }
 #pragma unroll
-      for (int cb = 0; cb < CB; ++cb) {
-        const int c = c0 + cb;
-        const int r = (lane + 32 * c) * PAIR;
-        if (!(c < CNT && (CH % 32 == 0 || lane + 32 * c < CH))) continue;
-        const int v = r / NPE, n = r - v * NPE;
-        const int sa = (el * NV + v) * LP + G::sn(n);
-        double U0 = uu[cb].x, S0 = uu[cb].x;
+    for (int b = 0; b < CB; ++b) {
+      if (!ok[b]) continue;
+      const int j = j0 + b;
+      const int el = warp + NW * (j / CNT), c = j % CNT;
+      const int r = (lane + 32 * c) * PAIR;
+      const int v = r / NPE, n = r - v * NPE;
+      const int sa = (el * NV + v) * LP + G::sn(n);
+      double U0 = uu[b].x, S0 = uu[b].x;
+#pragma unroll
+      for (int t = 0; t < NU; ++t) {
+        if (p.amask >> t & 1) U0 = A::mac(U0, p.ca[t], kk[b][t].x);
+        if (last && (p.bmask >> t & 1)) S0 = A::mac(S0, p.cb[t], kk[b][t].x);
+      }
+      sU[sa] = U0;
+      if constexpr (PAIR == 2) {
+        double U1 = uu[b].y, S1 = uu[b].y;
 #pragma unroll
         for (int t = 0; t < NU; ++t) {
-          if (p.amask >> t & 1) U0 = A::mac(U0, p.ca[t], kk[cb][t].x);
-          if (last && (p.bmask >> t & 1)) S0 = A::mac(S0, p.cb[t], kk[cb][t].x);
+          if (p.amask >> t & 1) U1 = A::mac(U1, p.ca[t], kk[b][t].y);
+          if (last && (p.bmask >> t & 1)) S1 = A::mac(S1, p.cb[t], kk[b][t].y);
         }
-        sU[sa] = U0;
-        if (last) sS[sa] = S0;
-        if constexpr (PAIR == 2) {
-          double U1 = uu[cb].y, S1 = uu[cb].y;
-#pragma unroll
-          for (int t = 0; t < NU; ++t) {
-            if (p.amask >> t & 1) U1 = A::mac(U1, p.ca[t], kk[cb][t].y);
-            if (last && (p.bmask >> t & 1)) S1 = A::mac(S1, p.cb[t], kk[cb][t].y);
-          }
-          sU[sa + 1] = U1;  // n and n+1 share an x-line (N even)
-          if (last) sS[sa + 1] = S1;
-        }
+        sU[sa + 1] = U1;  // n and n+1 share an x-line (N even)
+        if (last) *reinterpret_cast<double2*>(p.out + ga[b]) = make_double2(S0, S1);
+      } else {
+        if (last) p.out[ga[b]] = S0;
       }
     }
   }
 
-  // halo: the face plane of each out-of-tile neighbour, one warp per face
-  // (always loaded, also when the periodic wrap lands inside the tile --
-  // the values are identical)
+  // halo: the face plane of each out-of-tile neighbour (always loaded, also
+  // when the periodic wrap lands inside the tile -- the values are identical)
   constexpr int HV = NV * L;              // values per face plane
-  constexpr int HC = (HV + 31) / 32;
+  constexpr int HC = (HV + 31) / 32;      // chunks per lane per face
   constexpr int NF0 = 2 * G::HF0, NF1 = DIM > 1 ? 2 * G::HF1 : 0, NF2 = DIM > 2 ? 2 * G::HF2 : 0;
+  constexpr int NF = NF0 + NF1 + NF2;
+  constexpr int FPW = (NF + NW - 1) / NW;
+  constexpr int HJ = FPW * HC;
+  constexpr int HB = CB0 < HJ ? CB0 : HJ;
   double* sH = smem + G::OFF_H;
-  for (int fq = warp; fq < NF0 + NF1 + NF2; fq += nwarps) {
-    int axis, f2;
-    if (fq < NF0) { axis = 0; f2 = fq; }
-    else if (fq < NF0 + NF1) { axis = 1; f2 = fq - NF0; }
-    else { axis = 2; f2 = fq - NF0 - NF1; }
-    const int nf = axis == 0 ? G::HF0 : (axis == 1 ? G::HF1 : G::HF2);
-    const int side = f2 / nf, f = f2 - side * nf;
-    int ex, ey, ez;
-    if (axis == 0) { ey = f % G::TY; ez = f / G::TY; ex = side ? tc.vx - 1 : 0; }
-    else if (axis == 1) { ex = f % G::TX; ez = f / G::TX; ey = side ? tc.vy - 1 : 0; }
-    else { ex = f % G::TX; ey = f / G::TX; ez = side ? tc.vz - 1 : 0; }
-    if (!(ex < tc.vx && ey < tc.vy && ez < tc.vz)) continue;
-    int c[3] = {tc.x0 + ex, tc.y0 + ey, tc.z0 + ez};
-    const int cn = p.cells[axis];
-    c[axis] = side ? (c[axis] + 1 == cn ? 0 : c[axis] + 1) : (c[axis] == 0 ? cn - 1 : c[axis] - 1);
-    const size_t gb = ((size_t)c[0] + (size_t)C0 * ((size_t)c[1] + (size_t)C1 * c[2])) * NV * NPE;
-    double* dst = sH + G::halo_off(axis) + (side * nf + f) * HV;
-    double hu[HC], hk[HC][NU > 0 ? NU : 1];
 #pragma unroll
-    for (int cc = 0; cc < HC; ++cc) {
+  for (int j0 = 0; j0 < HJ; j0 += HB) {
+    double hu[HB], hk[HB][NU > 0 ? NU : 1];
+    int hd[HB];
+    bool ok[HB];
+#pragma unroll
+    for (int b = 0; b < HB; ++b) {
+      const int j = j0 + b;
+      const int fq = warp + NW * (j / HC), cc = j % HC;
       const int q = lane + 32 * cc;  // q = v * L + t
-      if (HV % 32 == 0 || q < HV) {
-        const int v = q / L, t = q - v * L;
-        const size_t g = gb + (size_t)v * NPE + G::node(axis, t, side ? 0 : N - 1);
-        hu[cc] = __ldg(p.u + g);
+      int axis, f2;
+      if (fq < NF0) { axis = 0; f2 = fq; }
+      else if (fq < NF0 + NF1) { axis = 1; f2 = fq - NF0; }
+      else { axis = 2; f2 = fq - NF0 - NF1; }
+      const int nf = axis == 0 ? G::HF0 : (axis == 1 ? G::HF1 : G::HF2);
+      const int side = f2 / nf, f = f2 - side * nf;
+      int ex, ey, ez;
+      if (axis == 0) { ey = f % G::TY; ez = f / G::TY; ex = side ? tc.vx - 1 : 0; }
+      else if (axis == 1) { ex = f % G::TX; ez = f / G::TX; ey = side ? tc.vy - 1 : 0; }
+      else { ex = f % G::TX; ey = f / G::TX; ez = side ? tc.vz - 1 : 0; }
+      ok[b] = j < HJ && fq < NF && ex < tc.vx && ey < tc.vy && ez < tc.vz && (HV % 32 == 0 || q < HV);
+      int cc3[3] = {tc.x0 + ex, tc.y0 + ey, tc.z0 + ez};
+      const int cn = p.cells[axis];
+      cc3[axis] = side ? (cc3[axis] + 1 == cn ? 0 : cc3[axis] + 1) : (cc3[axis] == 0 ? cn - 1 : cc3[axis] - 1);
+      const size_t gb = ((size_t)cc3[0] + (size_t)C0 * ((size_t)cc3[1] + (size_t)C1 * cc3[2])) * NV * NPE;
+      const int v = q / L, t = q - v * L;
+      const size_t g = gb + (size_t)v * NPE + G::node(axis, t, side ? 0 : N - 1);
+      hd[b] = G::halo_off(axis) + (side * nf + f) * HV + q;
+      if (ok[b]) {
+        hu[b] = __ldg(p.u + g);
 #pragma unroll
-        for (int tt = 0; tt < NU; ++tt) hk[cc][tt] = __ldg(p.ku[tt] + g);
+        for (int tt = 0; tt < NU; ++tt) hk[b][tt] = __ldg(p.ku[tt] + g);
       }
     }
 #pragma unroll
-    for (int cc = 0; cc < HC; ++cc) {
-      const int q = lane + 32 * cc;
-      if (!(HV % 32 == 0 || q < HV)) continue;
-      double U0 = hu[cc];
+    for (int b = 0; b < HB; ++b) {
+      if (!ok[b]) continue;
+      double U0 = hu[b];
 #pragma unroll
       for (int tt = 0; tt < NU; ++tt)
-        if (p.amask >> tt & 1) U0 = A::mac(U0, p.ca[tt], hk[cc][tt]);
-      dst[q] = U0;
+        if (p.amask >> tt & 1) U0 = A::mac(U0, p.ca[tt], hk[b][tt]);
+      sH[hd[b]] = U0;
     }
   }
 }
@@ -424,7 +440,6 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   double* sT = smem + G::OFF_T;  // [DIM-1][TE][2][NT][L]
   double* sH = smem + G::OFF_H;  // halo
   double* sR = smem + G::OFF_R;  // [32]
-  double* sS = smem + G::OFF_S;  // [TE][NV][LP] (last stage)
 
   // padded shared slot of the node at position k along `axis` of line tr:
   // sbase(axis) + k * sstride(axis)
@@ -622,8 +637,6 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   constexpr int FA = DIM - 1;  // axis of the final owner
   double alpha = 0.0;
   if (valid) {
-    const int sb = el * NV * LP + sbase(FA);
-    const int ss = sstride(FA);
     double* gout = p.out + ebase + gbase(FA);
     const int gs = gstride(FA);
 #pragma unroll
@@ -639,7 +652,8 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         bool finite = true;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          un[v] = A::mac(sS[sb + v * LP + k * ss], p.b_last, kv[v]);  // u += b_i k_i (solver.hpp:69-75)
+          // S was stored into this slot by the prepass of this CTA (a plain load, not __ldg)
+          un[v] = A::mac(gout[v * NPE + k * gs], p.b_last, kv[v]);  // u += b_i k_i (solver.hpp:69-75)
           gout[v * NPE + k * gs] = un[v];
           finite = finite && isfinite(un[v]);
         }
