@@ -279,7 +279,11 @@ __device__ __forceinline__ void prepass(const StageArgs& p, const TileCtx& tc, d
   constexpr int CNT = (CH + 31) / 32;      // chunks per lane per element
   constexpr int EPW = (TE + NW - 1) / NW;  // elements per warp
   constexpr int J = EPW * CNT;             // work items per lane
-  constexpr int CB0 = 8 / (1 + NU) < 1 ? 1 : 8 / (1 + NU);
+  // the prepass runs before the register-heavy line phases: spend the
+  // kernel's register allowance on loads in flight (4 registers per double2)
+  constexpr int REGCAP = 65536 / (G::THREADS * G::MINB) > 255 ? 255 : 65536 / (G::THREADS * G::MINB);
+  constexpr int BUDGET = (REGCAP - 48) / 4 < 2 ? 2 : (REGCAP - 48) / 4;
+  constexpr int CB0 = BUDGET / (1 + NU) < 1 ? 1 : BUDGET / (1 + NU);
   constexpr int CB = CB0 < J ? CB0 : J;    // items per load batch
   static_assert(NW >= 1, "stage kernel needs at least one full warp");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
