@@ -259,6 +259,36 @@ struct TileCtx {
   int vx, vy, vz;     // valid extent of the tile along each axis
 };
 
+// TMA bulk prefetch of [p, p+bytes) into L2 (sm_90+), 16-byte granular.
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  const size_t a0 = reinterpret_cast<size_t>(p) & ~size_t(15);
+  const size_t a1 = (reinterpret_cast<size_t>(p) + bytes + 15) & ~size_t(15);
+  size_t a = a0;
+  while (a < a1) {
+    const unsigned n = (unsigned)((a1 - a) > (size_t)(1u << 20) ? (1u << 20) : (a1 - a));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+    a += n;
+  }
+}
+
+// Prefetch the input rows (u and the union terms) of tile `tile` into L2.
+template <int DIM, int N, int KIND>
+__device__ __forceinline__ void prefetch_tile(const StageArgs& p, int tile) {
+  using G = Geo<DIM, N, KIND>;
+  constexpr int NV = G::NV, NPE = G::NPE;
+  const int C0 = p.cells[0], C1 = p.cells[1], C2 = p.cells[2];
+  const int ntx = (C0 + G::TX - 1) / G::TX, nty = (C1 + G::TY - 1) / G::TY;
+  const int x0 = (tile % ntx) * G::TX, y0 = ((tile / ntx) % nty) * G::TY, z0 = (tile / (ntx * nty)) * G::TZ;
+  const int vx = min(G::TX, C0 - x0), vy = min(G::TY, C1 - y0), vz = min(G::TZ, C2 - z0);
+  const size_t row_bytes = (size_t)vx * NV * NPE * sizeof(double);
+  for (int r = 0; r < vy * vz; ++r) {
+    const int y = y0 + r % vy, z = z0 + r / vy;
+    const size_t off = ((size_t)x0 + (size_t)C0 * ((size_t)y + (size_t)C1 * z)) * NV * NPE;
+    prefetch_l2(p.u + off, row_bytes);
+    for (int t = 0; t < p.nu; ++t) prefetch_l2(p.ku[t] + off, row_bytes);
+  }
+}
+
 // ------------------------------------------------------------ prepass
 // Node-parallel, coalesced, all terms in flight: U_s = u + sum a_sj K_j for
 // every node of the tile into padded shared memory, and at the last stage
@@ -417,7 +447,16 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 
   const int C0 = p.cells[0], C1 = p.cells[1], C2 = p.cells[2];
   const int ntx = (C0 + G::TX - 1) / G::TX, nty = (C1 + G::TY - 1) / G::TY;
-  const int bid = blockIdx.x;
+  const int ntiles = ntx * nty * ((C2 + G::TZ - 1) / G::TZ);
+  const double dt = p.rhs_only ? 1.0 : ctl->dt;
+  const long long step = p.rhs_only ? 0 : ctl->steps;
+  double alpha = 0.0;  // running max wavespeed of this CTA (last stage)
+  if (threadIdx.x == 0 && blockIdx.x < ntiles) prefetch_tile<DIM, N, KIND>(p, blockIdx.x);
+
+  // persistent CTAs: tiles bid, bid + grid, ...; the next tile's inputs are
+  // prefetched into L2 by TMA while this one computes
+  for (int bid = blockIdx.x; bid < ntiles; bid += gridDim.x) {
+  if (threadIdx.x == 0 && bid + (int)gridDim.x < ntiles) prefetch_tile<DIM, N, KIND>(p, bid + gridDim.x);
   TileCtx tc;
   tc.x0 = (bid % ntx) * G::TX;
   tc.y0 = ((bid / ntx) % nty) * G::TY;
@@ -436,14 +475,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   const size_t ebase = e * NV * NPE;
   const int tj = DIM > 1 ? tr % N : 0, tk = DIM > 2 ? tr / N : 0;  // x-line's (j, k)
 
-  const double dt = p.rhs_only ? 1.0 : ctl->dt;
-  const long long step = p.rhs_only ? 0 : ctl->steps;
-
   double* sU = smem + G::OFF_U;  // [TE][NV][LP]  U_s, then P
   double* sF = smem + G::OFF_F;  // [DIM-1][TE][NV][LP]
   double* sT = smem + G::OFF_T;  // [DIM-1][TE][2][NT][L]
   double* sH = smem + G::OFF_H;  // halo
-  double* sR = smem + G::OFF_R;  // [32]
 
   // padded shared slot of the node at position k along `axis` of line tr:
   // sbase(axis) + k * sstride(axis)
@@ -639,7 +674,6 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 
   // ------------------------------------------------------------ epilogue
   constexpr int FA = DIM - 1;  // axis of the final owner
-  double alpha = 0.0;
   if (valid) {
     double* gout = p.out + ebase + gbase(FA);
     const int gs = gstride(FA);
@@ -677,7 +711,11 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       }
     }
   }
+  __syncthreads();  // shared memory is reused by the next tile
+  }  // tile loop
+
   if (KIND == 1 && p.is_last && p.scan_alpha) {
+    double* sR = smem + G::OFF_R;
     // block max of the non-negative wavespeeds on their IEEE bit patterns
     // (valid for partial warps), then one global atomic per CTA
     unsigned long long* red = reinterpret_cast<unsigned long long*>(sR);

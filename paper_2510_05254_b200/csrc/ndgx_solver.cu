@@ -74,6 +74,7 @@ struct ndgx_solver {
   double K[3][64]{}, lift[3]{}, a[7][7]{}, b[7]{};
   double cflh = 0.0, two_n_minus_1 = 0.0, const_alpha = -1.0;
   ndgx::StageKernel kern;
+  int resident_ctas = 0;  // SMs x co-resident stage CTAs per SM
   cudaStream_t stream = nullptr;
   std::vector<double*> buf;
   int dead = -1;      // K slot overwritten by u_new at the last stage (-1: none)
@@ -144,9 +145,11 @@ struct ndgx_solver {
   }
 
   void launch_stage(const StageArgs& s) const {
-    const long long grid = (long long)((cells[0] + kern.tile[0] - 1) / kern.tile[0]) *
-                           ((cells[1] + kern.tile[1] - 1) / kern.tile[1]) *
-                           ((cells[2] + kern.tile[2] - 1) / kern.tile[2]);
+    const long long tiles = (long long)((cells[0] + kern.tile[0] - 1) / kern.tile[0]) *
+                            ((cells[1] + kern.tile[1] - 1) / kern.tile[1]) *
+                            ((cells[2] + kern.tile[2] - 1) / kern.tile[2]);
+    // persistent CTAs: as many as are co-resident, each walks tiles
+    const long long grid = std::min<long long>(tiles, (long long)resident_ctas);
     const int smem = s.is_last ? kern.smem_last : kern.smem_base;
     kern.fn<<<(unsigned)grid, kern.threads, smem, stream>>>(s);
   }
@@ -415,6 +418,13 @@ int ndgx_create(const ndgx_problem* prob, ndgx_solver** out, ndgx_error* err) {
     ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(s->kern.fn),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, s->kern.smem_last),
        "smem attribute");
+    {
+      int per_sm = 0;
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(s->kern.fn),
+                                                       s->kern.threads, s->kern.smem_last),
+         "occupancy");
+      s->resident_ctas = std::max(1, per_sm) * prop.multiProcessorCount;
+    }
     ck(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&s->ev0), "event");
     ck(cudaEventCreate(&s->ev1), "event");
