@@ -26,8 +26,13 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
          "-I", INCLUDE, "-I", CSRC]
 
-SOURCES = ["ndgx_inst_d1.cu", "ndgx_inst_d2.cu", "ndgx_inst_d3.cu", "ndgx_solver.cu",
-           "ndgx_setup.cpp"]
+# (source, object name, extra defines): the stage kernels are instantiated
+# once per (dim, order, arithmetic) so the objects compile in parallel
+SOURCES = [("ndgx_solver.cu", "ndgx_solver", []), ("ndgx_registry.cu", "ndgx_registry", []),
+           ("ndgx_setup.cpp", "ndgx_setup", [])] + [
+    ("ndgx_inst.cu", f"ndgx_inst_d{d}_o{n}_e{e}",
+     [f"-DNDGX_DIM={d}", f"-DNDGX_ORDER={n}", f"-DNDGX_EXACT={e}"])
+    for d in (1, 2, 3) for n in range(2, 9) for e in (0, 1)]
 HEADERS = ["ndgx_device.cuh", "ndgx_kernels.h", "ndgx_setup.h"]
 
 
@@ -39,11 +44,12 @@ def _stale(obj: str, src: str) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+def _compile(item) -> str:
+    src, name, defs = item
+    obj = os.path.join(BUILD, name + ".o")
     path = os.path.join(CSRC, src)
     if _stale(obj, path):
-        cmd = [NVCC] + ARCH + FLAGS + ["-c", path, "-o", obj]
+        cmd = [NVCC] + ARCH + FLAGS + defs + ["-c", path, "-o", obj]
         if src.endswith(".cpp"):
             cxx = os.environ.get("CXX", shutil.which("g++") or "g++")
             cmd = [cxx, "-O2", "-fPIC", "-ffp-contract=off", "-std=c++17", "-I", INCLUDE, "-I", CSRC,
@@ -59,8 +65,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force:
         for f in os.listdir(BUILD):
             os.remove(os.path.join(BUILD, f))
-    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(_compile, SOURCES))
+    # the heaviest objects (3D and high orders) first
+    order = sorted(SOURCES, key=lambda it: -sum(int(d.split("=")[1]) for d in it[2][:2]) if it[2] else 0)
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        done = dict(zip([it[1] for it in order], ex.map(_compile, order)))
+    objs = [done[it[1]] for it in SOURCES]
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)

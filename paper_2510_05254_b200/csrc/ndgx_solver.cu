@@ -74,7 +74,7 @@ struct ndgx_solver {
   double K[3][64]{}, lift[3]{}, a[7][7]{}, b[7]{};
   double cflh = 0.0, two_n_minus_1 = 0.0, const_alpha = -1.0;
   ndgx::StageKernel kern;
-  int resident_ctas = 0;  // SMs x co-resident stage CTAs per SM
+  ndgx::StageLaunch lcfg[ndgx::kMaxTerms + 1];  // per number of K_j terms a stage reads
   cudaStream_t stream = nullptr;
   std::vector<double*> buf;
   int dead = -1;      // K slot overwritten by u_new at the last stage (-1: none)
@@ -141,6 +141,8 @@ struct ndgx_solver {
       for (int q = 0; q < 64; ++q) s.K[d][q] = K[d][q];
     }
     s.sound_speed = p.sound_speed;
+    s.depth = lcfg[s.nu].depth;
+    s.ring_main = lcfg[s.nu].ring_main;
     return s;
   }
 
@@ -149,9 +151,9 @@ struct ndgx_solver {
                             ((cells[1] + kern.tile[1] - 1) / kern.tile[1]) *
                             ((cells[2] + kern.tile[2] - 1) / kern.tile[2]);
     // persistent CTAs: as many as are co-resident, each walks tiles
-    const long long grid = std::min<long long>(tiles, (long long)resident_ctas);
-    const int smem = s.is_last ? kern.smem_last : kern.smem_base;
-    kern.fn<<<(unsigned)grid, kern.threads, smem, stream>>>(s);
+    const ndgx::StageLaunch& c = lcfg[s.nu];
+    const long long grid = std::max<long long>(1, std::min<long long>(tiles, (long long)c.grid));
+    kern.fn<<<(unsigned)grid, kern.threads, c.smem, stream>>>(s);
   }
 
   StepParams step_params(Control* c, long long fixed, int warmup) const {
@@ -217,6 +219,58 @@ struct ndgx_solver {
     }
     graph_fixed = fixed;
     graph_tend = p.t_end;
+  }
+
+  // Ring configuration per term count: the deepest ring that fits, TMA-staged
+  // tile arrays when the element rows allow bulk copies; grid = co-resident CTAs.
+  int configure_launches(const cudaDeviceProp& prop, ndgx_error* err) {
+    const void* fn = reinterpret_cast<const void*>(kern.fn);
+    const int limit = (int)prop.sharedMemPerBlockOptin;
+    int max_smem = 0;
+    for (int nu = 0; nu <= ndgx::kMaxTerms; ++nu) {
+      ndgx::StageLaunch c;
+      bool found = false;
+      for (int main = kern.tma_ok ? 1 : 0; main >= 0 && !found; --main)
+        for (int depth = 2; depth >= 1 && !found; --depth) {
+          const long long bytes = (long long)kern.fixed_bytes +
+                                  (long long)depth * ((main ? (1 + nu) * (long long)kern.tile_arr_bytes : 0) +
+                                                      kern.halo_bytes + (1 + nu) * (long long)kern.raw_bytes);
+          if (bytes <= limit) {
+            c.depth = depth;
+            c.ring_main = main;
+            c.smem = (int)bytes;
+            found = true;
+          }
+        }
+      if (!found) {
+        if (nu == 0) {
+          set_error(err, NDGX_ERR_CONFIG, "stage kernel does not fit in shared memory");
+          return NDGX_ERR_CONFIG;
+        }
+        c = lcfg[nu - 1];
+        c.grid = 0;  // unusable: create() rejects tableaus that need it
+      }
+      lcfg[nu] = c;
+      if (found) max_smem = std::max(max_smem, c.smem);
+    }
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem), "smem attribute");
+    for (int nu = 0; nu <= ndgx::kMaxTerms; ++nu) {
+      if (lcfg[nu].grid == 0) continue;
+      int per_sm = 0;
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kern.threads, lcfg[nu].smem), "occupancy");
+      lcfg[nu].grid = std::max(1, per_sm) * prop.multiProcessorCount;
+    }
+    // every stage of this tableau must have a configuration
+    for (int i = 0; i < stages; ++i) {
+      int nu = 0;
+      for (int j = 0; j < i; ++j)
+        if (a[i][j] != 0.0 || (i == stages - 1 && b[j] != 0.0)) ++nu;
+      if (lcfg[nu].grid == 0) {
+        set_error(err, NDGX_ERR_CONFIG, "stage kernel ring does not fit in shared memory");
+        return NDGX_ERR_CONFIG;
+      }
+    }
+    return NDGX_OK;
   }
 
   // device index of (AoS cell index, AoS node key, var)
@@ -415,15 +469,9 @@ int ndgx_create(const ndgx_problem* prob, ndgx_solver** out, ndgx_error* err) {
       set_error(err, NDGX_ERR_CONFIG, "no GPU kernel for this (dim, order, equation)");
       return NDGX_ERR_CONFIG;
     }
-    ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(s->kern.fn),
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, s->kern.smem_last),
-       "smem attribute");
-    {
-      int per_sm = 0;
-      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(s->kern.fn),
-                                                       s->kern.threads, s->kern.smem_last),
-         "occupancy");
-      s->resident_ctas = std::max(1, per_sm) * prop.multiProcessorCount;
+    if (int rc = s->configure_launches(prop, err)) {
+      delete s;
+      return rc;
     }
     ck(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&s->ev0), "event");
@@ -670,12 +718,3 @@ int ndgx_profile_step(ndgx_solver* s, float* ms, int n, ndgx_error* err) {
 }
 
 }  // extern "C"
-
-namespace ndgx {
-StageKernel find_stage_kernel(int dim, int order, int kind, bool exact) {
-  if (dim == 1) return find_stage_kernel_d1(order, kind, exact);
-  if (dim == 2) return find_stage_kernel_d2(order, kind, exact);
-  if (dim == 3) return find_stage_kernel_d3(order, kind, exact);
-  return StageKernel{};
-}
-}  // namespace ndgx
