@@ -33,7 +33,7 @@ SOURCES = [("ndgx_solver.cu", "ndgx_solver", []), ("ndgx_registry.cu", "ndgx_reg
     ("ndgx_inst.cu", f"ndgx_inst_d{d}_o{n}_e{e}",
      [f"-DNDGX_DIM={d}", f"-DNDGX_ORDER={n}", f"-DNDGX_EXACT={e}"])
     for d in (1, 2, 3) for n in range(2, 9) for e in (0, 1)]
-HEADERS = ["ndgx_device.cuh", "ndgx_kernels.h", "ndgx_setup.h"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 
 def _stale(obj: str, src: str) -> bool:

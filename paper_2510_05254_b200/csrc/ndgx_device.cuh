@@ -24,6 +24,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace ndgx {
@@ -130,9 +131,11 @@ struct Ar<false> {  // contracted
 __device__ __forceinline__ double dmax(double a, double b) { return (a < b) ? b : a; }
 
 // F_axis(u) and the one-sided wavespeed bound (models.cpp:42-70).
+// With rinv >= 0 (contracted mode only) u_a / rho is formed as u_a * (1 / rho),
+// sharing one reciprocal between the axes of a node.
 template <int DIM, int KIND, bool EXACT>
 __device__ __forceinline__ void flux(const StageArgs& p, const double* u, int axis, double* f,
-                                     double& speed) {
+                                     double& speed, double rinv = -1.0) {
   using A = Ar<EXACT>;
   if (KIND == 0) {
     f[0] = A::mul(p.vel[axis], u[0]);
@@ -140,7 +143,7 @@ __device__ __forceinline__ void flux(const StageArgs& p, const double* u, int ax
   } else {
     constexpr int NV = DIM + 1;
     const double rho = u[0];
-    const double ua = A::div(u[1 + axis], rho);
+    const double ua = (!EXACT && rinv >= 0.0) ? u[1 + axis] * rinv : A::div(u[1 + axis], rho);
     f[0] = u[1 + axis];
 #pragma unroll
     for (int i = 1; i < NV; ++i) f[i] = A::mul(ua, u[i]);

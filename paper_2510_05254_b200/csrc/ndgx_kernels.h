@@ -22,7 +22,7 @@ struct StageKernel {
 
 // Ring configuration of one stage launch (host side).
 struct StageLaunch {
-  int depth = 1, ring_main = 0, smem = 0, grid = 1;
+  int ring_main = 0, dm = 1, dh = 1, smem = 0, grid = 1;
 };
 
 // dim 1..3, order 2..8, kind 0 advection / 1 Euler, exact arithmetic or FMA-contracted

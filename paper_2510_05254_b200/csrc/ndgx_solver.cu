@@ -110,17 +110,21 @@ struct ndgx_solver {
     s.is_last = (!rhs_only && i == stages - 1) ? 1 : 0;
     // union (ascending j) of the K_j read by the stage input (a_ij != 0,
     // solver.hpp:58) and, at the last stage, by S (b_j != 0, solver.hpp:71)
-    s.nu = 0;
+    s.nu = s.nA = s.nB = 0;
     for (int j = 0; j < i; ++j) {
       const bool ua = a[i][j] != 0.0;
       const bool ub = s.is_last && b[j] != 0.0;
       if (!ua && !ub) continue;
       s.ku[s.nu] = k_buf(j, par);
-      s.ca[s.nu] = a[i][j];
-      s.cb[s.nu] = b[j];
-      if (ua) s.amask |= 1 << s.nu;
-      if (ub) s.bmask |= 1 << s.nu;
-      ++s.nu;
+      ++s.nu;  // ring/input array index s.nu (0 is u)
+      if (ua) {
+        s.ia[s.nA] = s.nu;
+        s.ca[s.nA++] = a[i][j];
+      }
+      if (ub) {
+        s.ib[s.nB] = s.nu;
+        s.cb[s.nB++] = b[j];
+      }
     }
     if (s.is_last) {
       s.b_last = b[i];
@@ -141,8 +145,9 @@ struct ndgx_solver {
       for (int q = 0; q < 64; ++q) s.K[d][q] = K[d][q];
     }
     s.sound_speed = p.sound_speed;
-    s.depth = lcfg[s.nu].depth;
     s.ring_main = lcfg[s.nu].ring_main;
+    s.dm = lcfg[s.nu].dm;
+    s.dh = lcfg[s.nu].dh;
     return s;
   }
 
@@ -230,18 +235,23 @@ struct ndgx_solver {
     for (int nu = 0; nu <= ndgx::kMaxTerms; ++nu) {
       ndgx::StageLaunch c;
       bool found = false;
-      for (int main = kern.tma_ok ? 1 : 0; main >= 0 && !found; --main)
-        for (int depth = 2; depth >= 1 && !found; --depth) {
-          const long long bytes = (long long)kern.fixed_bytes +
-                                  (long long)depth * ((main ? (1 + nu) * (long long)kern.tile_arr_bytes : 0) +
-                                                      kern.halo_bytes + (1 + nu) * (long long)kern.raw_bytes);
-          if (bytes <= limit) {
-            c.depth = depth;
-            c.ring_main = main;
-            c.smem = (int)bytes;
-            found = true;
-          }
+      // (main ring, main depth, halo depth), best first
+      // (the producer runs one tile ahead, so the halo ring needs >= 2 slots)
+      static const int opts[][3] = {{1, 2, 3}, {1, 2, 2}, {1, 1, 3}, {1, 1, 2}, {0, 0, 3}, {0, 0, 2}};
+      for (const auto& o : opts) {
+        if (o[0] && !kern.tma_ok) continue;
+        const long long bytes = (long long)kern.fixed_bytes +
+                                (long long)o[1] * (1 + nu) * (long long)kern.tile_arr_bytes +
+                                (long long)o[2] * (kern.halo_bytes + (1 + nu) * (long long)kern.raw_bytes);
+        if (bytes <= limit) {
+          c.ring_main = o[0];
+          c.dm = std::max(1, o[1]);
+          c.dh = o[2];
+          c.smem = (int)bytes;
+          found = true;
+          break;
         }
+      }
       if (!found) {
         if (nu == 0) {
           set_error(err, NDGX_ERR_CONFIG, "stage kernel does not fit in shared memory");

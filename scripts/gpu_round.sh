@@ -4,8 +4,9 @@
 TAG=${1:-dev}; NCU=${2:-none}; AR=${3:-exact}
 OUT=gpurun_out/$TAG; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > $OUT/smi.txt 2>&1
-timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log; tail -3 $OUT/smoke.log
-timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest.log
+timeout 90 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; RC=$?; echo "smoke rc=$RC" >> $OUT/smoke.log; tail -3 $OUT/smoke.log
+if [ $RC -ne 0 ]; then echo "smoke failed: skipping the rest"; exit 1; fi
+timeout 300 python -m pytest tests -m gpu -x -q --timeout 60 > $OUT/pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest.log
 tail -5 $OUT/pytest.log
 timeout 400 python scripts/quickbench.py > $OUT/quick.log 2>&1; tail -8 $OUT/quick.log
 if [ "$NCU" != "none" ]; then
