@@ -72,13 +72,12 @@ struct StepParams {
 
 struct StageArgs {
   const double* u;                 // u^n
-  // ku[0..nu): the K_j this stage reads (ascending j) -- ring arrays 1..nu.
-  // Stage input U_s = u + sum_t ca[t] * arr[ia[t]] over the nA terms with
-  // a_sj != 0 (solver.hpp:55-62); at the last stage S = u + sum_t cb[t] *
-  // arr[ib[t]] over the nB terms with b_j != 0 (solver.hpp:69-75); both in j order.
+  // ku[0..nu): the K_j this stage reads (ascending j).  Stage input U_s =
+  // u + sum over t with bit t of amask of ca[t] * ku[t] (a_sj != 0,
+  // solver.hpp:55-62); at the last stage S = u + sum over bit t of bmask of
+  // cb[t] * ku[t] (b_j != 0, solver.hpp:69-75); both in ascending j order.
   const double* ku[kMaxTerms];
-  int nu, nA, nB;
-  int ia[kMaxTerms], ib[kMaxTerms];
+  int nu, amask, bmask;
   double ca[kMaxTerms], cb[kMaxTerms];
   double* out;                     // K_s, or u_new at the last stage
   Control* ctl;
@@ -94,8 +93,6 @@ struct StageArgs {
   double vel[3];
   double lift[3];
   double K[3][kMaxOrder * kMaxOrder];  // K_d[k*N + l] (solver.cpp:203-207)
-  int ring_main;                   // 1: TMA-stage u and the K_j tiles in the main ring
-  int dm, dh;                      // main / halo ring depths
   // multi-block: stage-input face planes received from the neighbour across
   // [axis][side] (side 0 low, 1 high), layout [cross-section cell][var][face node];
   // null -> periodic wrap inside this block

@@ -10,19 +10,10 @@ namespace ndgx {
 using StageFn = void (*)(const StageArgs);
 
 struct StageKernel {
-  StageFn fn = nullptr;
+  StageFn fn[kMaxTerms + 1] = {};  // by the number of K_j a stage reads
   int threads = 0;
-  int tile[3] = {1, 1, 1};  // elements per CTA tile along x, y, z
-  int fixed_bytes = 0;      // mbarriers + work area (dynamic shared memory)
-  int tile_arr_bytes = 0;   // one ring copy of a tile array (u or one K_j)
-  int halo_bytes = 0;       // one ring slot's face halo records
-  int raw_bytes = 0;        // one ring slot's raw halo values per input array
-  bool tma_ok = false;      // element rows are 16-byte multiples (bulk copies)
-};
-
-// Ring configuration of one stage launch (host side).
-struct StageLaunch {
-  int ring_main = 0, dm = 1, dh = 1, smem = 0, grid = 1;
+  int warps = 0;  // elements in flight per CTA (one per warp)
+  int smem = 0;   // dynamic shared memory (warp-private slabs)
 };
 
 // dim 1..3, order 2..8, kind 0 advection / 1 Euler, exact arithmetic or FMA-contracted
@@ -32,16 +23,16 @@ template <int DIM, int N, int KIND, bool EXACT>
 StageKernel make_stage_kernel() {
   using G = Geo<DIM, N, KIND>;
   StageKernel k;
-  k.fn = &stage_kernel<DIM, N, KIND, EXACT>;
+  k.fn[0] = &stage_kernel<DIM, N, KIND, EXACT, 0>;
+  k.fn[1] = &stage_kernel<DIM, N, KIND, EXACT, 1>;
+  k.fn[2] = &stage_kernel<DIM, N, KIND, EXACT, 2>;
+  k.fn[3] = &stage_kernel<DIM, N, KIND, EXACT, 3>;
+  k.fn[4] = &stage_kernel<DIM, N, KIND, EXACT, 4>;
+  k.fn[5] = &stage_kernel<DIM, N, KIND, EXACT, 5>;
+  k.fn[6] = &stage_kernel<DIM, N, KIND, EXACT, 6>;
   k.threads = G::THREADS;
-  k.tile[0] = G::TX;
-  k.tile[1] = G::TY;
-  k.tile[2] = G::TZ;
-  k.fixed_bytes = G::BAR_BYTES + G::WORK * 8;
-  k.tile_arr_bytes = G::TILE_ARR * 8;
-  k.halo_bytes = G::HALO * 8;
-  k.raw_bytes = G::RAW1 * 8;
-  k.tma_ok = G::TMA_OK;
+  k.warps = G::WARPS;
+  k.smem = G::SMEM;
   return k;
 }
 

@@ -74,7 +74,7 @@ struct ndgx_solver {
   double K[3][64]{}, lift[3]{}, a[7][7]{}, b[7]{};
   double cflh = 0.0, two_n_minus_1 = 0.0, const_alpha = -1.0;
   ndgx::StageKernel kern;
-  ndgx::StageLaunch lcfg[ndgx::kMaxTerms + 1];  // per number of K_j terms a stage reads
+  int resident = 0;  // co-resident stage CTAs (all SMs)
   cudaStream_t stream = nullptr;
   std::vector<double*> buf;
   int dead = -1;      // K slot overwritten by u_new at the last stage (-1: none)
@@ -110,21 +110,17 @@ struct ndgx_solver {
     s.is_last = (!rhs_only && i == stages - 1) ? 1 : 0;
     // union (ascending j) of the K_j read by the stage input (a_ij != 0,
     // solver.hpp:58) and, at the last stage, by S (b_j != 0, solver.hpp:71)
-    s.nu = s.nA = s.nB = 0;
+    s.nu = 0;
     for (int j = 0; j < i; ++j) {
       const bool ua = a[i][j] != 0.0;
       const bool ub = s.is_last && b[j] != 0.0;
       if (!ua && !ub) continue;
       s.ku[s.nu] = k_buf(j, par);
-      ++s.nu;  // ring/input array index s.nu (0 is u)
-      if (ua) {
-        s.ia[s.nA] = s.nu;
-        s.ca[s.nA++] = a[i][j];
-      }
-      if (ub) {
-        s.ib[s.nB] = s.nu;
-        s.cb[s.nB++] = b[j];
-      }
+      s.ca[s.nu] = a[i][j];
+      s.cb[s.nu] = b[j];
+      if (ua) s.amask |= 1 << s.nu;
+      if (ub) s.bmask |= 1 << s.nu;
+      ++s.nu;
     }
     if (s.is_last) {
       s.b_last = b[i];
@@ -145,20 +141,15 @@ struct ndgx_solver {
       for (int q = 0; q < 64; ++q) s.K[d][q] = K[d][q];
     }
     s.sound_speed = p.sound_speed;
-    s.ring_main = lcfg[s.nu].ring_main;
-    s.dm = lcfg[s.nu].dm;
-    s.dh = lcfg[s.nu].dh;
     return s;
   }
 
   void launch_stage(const StageArgs& s) const {
-    const long long tiles = (long long)((cells[0] + kern.tile[0] - 1) / kern.tile[0]) *
-                            ((cells[1] + kern.tile[1] - 1) / kern.tile[1]) *
-                            ((cells[2] + kern.tile[2] - 1) / kern.tile[2]);
-    // persistent CTAs: as many as are co-resident, each walks tiles
-    const ndgx::StageLaunch& c = lcfg[s.nu];
-    const long long grid = std::max<long long>(1, std::min<long long>(tiles, (long long)c.grid));
-    kern.fn<<<(unsigned)grid, kern.threads, c.smem, stream>>>(s);
+    // persistent CTAs (one element per warp): as many as are co-resident
+    const long long warps = (long long)cells[0] * cells[1] * cells[2];
+    const long long need = (warps + kern.warps - 1) / kern.warps;
+    const long long grid = std::max<long long>(1, std::min<long long>(need, (long long)resident));
+    kern.fn[s.nu]<<<(unsigned)grid, kern.threads, kern.smem, stream>>>(s);
   }
 
   StepParams step_params(Control* c, long long fixed, int warmup) const {
@@ -226,59 +217,20 @@ struct ndgx_solver {
     graph_tend = p.t_end;
   }
 
-  // Ring configuration per term count: the deepest ring that fits, TMA-staged
-  // tile arrays when the element rows allow bulk copies; grid = co-resident CTAs.
+  // Co-resident CTAs of the stage kernel (grid of the persistent launch).
   int configure_launches(const cudaDeviceProp& prop, ndgx_error* err) {
-    const void* fn = reinterpret_cast<const void*>(kern.fn);
-    const int limit = (int)prop.sharedMemPerBlockOptin;
-    int max_smem = 0;
-    for (int nu = 0; nu <= ndgx::kMaxTerms; ++nu) {
-      ndgx::StageLaunch c;
-      bool found = false;
-      // (main ring, main depth, halo depth), best first
-      // (the producer runs one tile ahead, so the halo ring needs >= 2 slots)
-      static const int opts[][3] = {{1, 2, 3}, {1, 2, 2}, {1, 1, 3}, {1, 1, 2}, {0, 0, 3}, {0, 0, 2}};
-      for (const auto& o : opts) {
-        if (o[0] && !kern.tma_ok) continue;
-        const long long bytes = (long long)kern.fixed_bytes +
-                                (long long)o[1] * (1 + nu) * (long long)kern.tile_arr_bytes +
-                                (long long)o[2] * (kern.halo_bytes + (1 + nu) * (long long)kern.raw_bytes);
-        if (bytes <= limit) {
-          c.ring_main = o[0];
-          c.dm = std::max(1, o[1]);
-          c.dh = o[2];
-          c.smem = (int)bytes;
-          found = true;
-          break;
-        }
-      }
-      if (!found) {
-        if (nu == 0) {
-          set_error(err, NDGX_ERR_CONFIG, "stage kernel does not fit in shared memory");
-          return NDGX_ERR_CONFIG;
-        }
-        c = lcfg[nu - 1];
-        c.grid = 0;  // unusable: create() rejects tableaus that need it
-      }
-      lcfg[nu] = c;
-      if (found) max_smem = std::max(max_smem, c.smem);
+    if (kern.smem > (int)prop.sharedMemPerBlockOptin) {
+      set_error(err, NDGX_ERR_CONFIG, "stage kernel does not fit in shared memory");
+      return NDGX_ERR_CONFIG;
     }
-    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem), "smem attribute");
+    resident = 0;
     for (int nu = 0; nu <= ndgx::kMaxTerms; ++nu) {
-      if (lcfg[nu].grid == 0) continue;
+      const void* fn = reinterpret_cast<const void*>(kern.fn[nu]);
+      ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kern.smem), "smem attribute");
       int per_sm = 0;
-      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kern.threads, lcfg[nu].smem), "occupancy");
-      lcfg[nu].grid = std::max(1, per_sm) * prop.multiProcessorCount;
-    }
-    // every stage of this tableau must have a configuration
-    for (int i = 0; i < stages; ++i) {
-      int nu = 0;
-      for (int j = 0; j < i; ++j)
-        if (a[i][j] != 0.0 || (i == stages - 1 && b[j] != 0.0)) ++nu;
-      if (lcfg[nu].grid == 0) {
-        set_error(err, NDGX_ERR_CONFIG, "stage kernel ring does not fit in shared memory");
-        return NDGX_ERR_CONFIG;
-      }
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kern.threads, kern.smem), "occupancy");
+      const int r = std::max(1, per_sm) * prop.multiProcessorCount;
+      resident = resident == 0 ? r : std::min(resident, r);
     }
     return NDGX_OK;
   }
@@ -474,7 +426,7 @@ int ndgx_create(const ndgx_problem* prob, ndgx_solver** out, ndgx_error* err) {
       }
 
     s->kern = ndgx::find_stage_kernel(s->dim, s->N, s->kind, s->exact);
-    if (!s->kern.fn) {
+    if (!s->kern.fn[0]) {
       delete s;
       set_error(err, NDGX_ERR_CONFIG, "no GPU kernel for this (dim, order, equation)");
       return NDGX_ERR_CONFIG;
