@@ -70,6 +70,17 @@ struct StepParams {
   int warmup;             // warm-up step: non-finite dt -> t_end, no stats
 };
 
+// Stage signatures of the supported tableaus (make_rk3/4/6, solver.cpp:17-68):
+// (number of K_j read, bit t set when ku[t] enters U_s (a != 0), bit t set
+// when ku[t] enters the last stage's S (b != 0)).  Kernels are instantiated
+// per signature so the term loops are fully resolved at compile time.
+struct StageSig {
+  int nu, am, bm;
+};
+constexpr StageSig kSigs[] = {{0, 0, 0},  {1, 1, 0},  {2, 2, 1},  {3, 4, 7},  {2, 3, 0},
+                              {3, 7, 0},  {4, 15, 0}, {5, 31, 0}, {6, 63, 53}};
+constexpr int kNumSigs = 9;
+
 struct StageArgs {
   const double* u;                 // u^n
   // ku[0..nu): the K_j this stage reads (ascending j).  Stage input U_s =
@@ -93,6 +104,8 @@ struct StageArgs {
   double vel[3];
   double lift[3];
   double K[3][kMaxOrder * kMaxOrder];  // K_d[k*N + l] (solver.cpp:203-207)
+  int depth;                       // per-warp ring depth (elements in flight + 1); 0: direct loads
+  int sig;                         // index into kSigs (host bookkeeping)
   // multi-block: stage-input face planes received from the neighbour across
   // [axis][side] (side 0 low, 1 high), layout [cross-section cell][var][face node];
   // null -> periodic wrap inside this block

@@ -10,10 +10,18 @@ namespace ndgx {
 using StageFn = void (*)(const StageArgs);
 
 struct StageKernel {
-  StageFn fn[kMaxTerms + 1] = {};  // by the number of K_j a stage reads
+  StageFn fn[kNumSigs] = {};  // by stage signature (kSigs)
   int threads = 0;
-  int warps = 0;  // elements in flight per CTA (one per warp)
-  int smem = 0;   // dynamic shared memory (warp-private slabs)
+  int warps = 0;            // elements in flight per CTA (one per warp)
+  int smem_fixed = 0;       // dynamic shared memory without the element rings
+  int ring_per_array = 0;   // ring bytes per slot per input array (all warps of a CTA)
+  bool tma_ok = false;      // element chunks are 16-byte multiples (bulk copies)
+  int smem(int nu, int depth) const { return smem_fixed + depth * (1 + nu) * ring_per_array; }
+};
+
+// Launch configuration of one stage kernel variant (host side).
+struct StageLaunch {
+  int depth = 0, smem = 0, grid = 1;
 };
 
 // dim 1..3, order 2..8, kind 0 advection / 1 Euler, exact arithmetic or FMA-contracted
@@ -30,9 +38,13 @@ StageKernel make_stage_kernel() {
   k.fn[4] = &stage_kernel<DIM, N, KIND, EXACT, 4>;
   k.fn[5] = &stage_kernel<DIM, N, KIND, EXACT, 5>;
   k.fn[6] = &stage_kernel<DIM, N, KIND, EXACT, 6>;
+  k.fn[7] = &stage_kernel<DIM, N, KIND, EXACT, 7>;
+  k.fn[8] = &stage_kernel<DIM, N, KIND, EXACT, 8>;
   k.threads = G::THREADS;
   k.warps = G::WARPS;
-  k.smem = G::SMEM;
+  k.smem_fixed = G::smem_bytes(0, 0);
+  k.ring_per_array = G::WARPS * G::CHUNK * 8;
+  k.tma_ok = G::TMA_OK;
   return k;
 }
 

@@ -74,7 +74,7 @@ struct ndgx_solver {
   double K[3][64]{}, lift[3]{}, a[7][7]{}, b[7]{};
   double cflh = 0.0, two_n_minus_1 = 0.0, const_alpha = -1.0;
   ndgx::StageKernel kern;
-  int resident = 0;  // co-resident stage CTAs (all SMs)
+  ndgx::StageLaunch lcfg[ndgx::kNumSigs];  // per stage signature (ndgx::kSigs)
   cudaStream_t stream = nullptr;
   std::vector<double*> buf;
   int dead = -1;      // K slot overwritten by u_new at the last stage (-1: none)
@@ -141,6 +141,8 @@ struct ndgx_solver {
       for (int q = 0; q < 64; ++q) s.K[d][q] = K[d][q];
     }
     s.sound_speed = p.sound_speed;
+    s.sig = sig_of(s);
+    s.depth = lcfg[s.sig].depth;
     return s;
   }
 
@@ -148,8 +150,9 @@ struct ndgx_solver {
     // persistent CTAs (one element per warp): as many as are co-resident
     const long long warps = (long long)cells[0] * cells[1] * cells[2];
     const long long need = (warps + kern.warps - 1) / kern.warps;
-    const long long grid = std::max<long long>(1, std::min<long long>(need, (long long)resident));
-    kern.fn[s.nu]<<<(unsigned)grid, kern.threads, kern.smem, stream>>>(s);
+    const ndgx::StageLaunch& c = lcfg[s.sig];
+    const long long grid = std::max<long long>(1, std::min<long long>(need, (long long)c.grid));
+    kern.fn[s.sig]<<<(unsigned)grid, kern.threads, c.smem, stream>>>(s);
   }
 
   StepParams step_params(Control* c, long long fixed, int warmup) const {
@@ -218,19 +221,59 @@ struct ndgx_solver {
   }
 
   // Co-resident CTAs of the stage kernel (grid of the persistent launch).
+  static int sig_of(const StageArgs& s) {
+    for (int q = 0; q < ndgx::kNumSigs; ++q)
+      if (ndgx::kSigs[q].nu == s.nu && ndgx::kSigs[q].am == s.amask && ndgx::kSigs[q].bm == s.bmask) return q;
+    return -1;
+  }
+
+  // Per stage signature: the per-warp ring depth (0 = direct loads) giving the
+  // most resident warps (the element pipeline is issue-bound), then the most
+  // elements in flight.
   int configure_launches(const cudaDeviceProp& prop, ndgx_error* err) {
-    if (kern.smem > (int)prop.sharedMemPerBlockOptin) {
-      set_error(err, NDGX_ERR_CONFIG, "stage kernel does not fit in shared memory");
-      return NDGX_ERR_CONFIG;
+    const int limit = (int)prop.sharedMemPerBlockOptin;
+    for (int i = 0; i < stages; ++i) {
+      StageArgs t;
+      std::memset(&t, 0, sizeof(t));
+      for (int j = 0; j < i; ++j) {
+        const bool ua = a[i][j] != 0.0, ub = i == stages - 1 && b[j] != 0.0;
+        if (!ua && !ub) continue;
+        if (ua) t.amask |= 1 << t.nu;
+        if (ub) t.bmask |= 1 << t.nu;
+        ++t.nu;
+      }
+      if (sig_of(t) < 0) {
+        set_error(err, NDGX_ERR_CONFIG, "Runge-Kutta tableau without a compiled stage signature");
+        return NDGX_ERR_CONFIG;
+      }
     }
-    resident = 0;
-    for (int nu = 0; nu <= ndgx::kMaxTerms; ++nu) {
-      const void* fn = reinterpret_cast<const void*>(kern.fn[nu]);
-      ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kern.smem), "smem attribute");
-      int per_sm = 0;
-      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kern.threads, kern.smem), "occupancy");
-      const int r = std::max(1, per_sm) * prop.multiProcessorCount;
-      resident = resident == 0 ? r : std::min(resident, r);
+    for (int q = 0; q < ndgx::kNumSigs; ++q) {
+      const int nu = ndgx::kSigs[q].nu;
+      const void* fn = reinterpret_cast<const void*>(kern.fn[q]);
+      ndgx::StageLaunch best;
+      long long best_score = -1;
+      for (int d = kern.tma_ok ? 4 : 0; d >= 0; --d) {
+        if (d == 1) continue;  // a ring needs one slot ahead
+        const int bytes = kern.smem(nu, d);
+        if (bytes > limit) continue;
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attribute");
+        int per_sm = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kern.threads, bytes), "occupancy");
+        if (per_sm < 1) continue;
+        const long long score = (long long)per_sm * kern.warps * 16 + std::max(1, d - 1);
+        if (score > best_score) {
+          best_score = score;
+          best.depth = d;
+          best.smem = bytes;
+          best.grid = per_sm * prop.multiProcessorCount;
+        }
+      }
+      if (best_score < 0) {
+        set_error(err, NDGX_ERR_CONFIG, "stage kernel does not fit in shared memory");
+        return NDGX_ERR_CONFIG;
+      }
+      ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, best.smem), "smem attribute");
+      lcfg[q] = best;
     }
     return NDGX_OK;
   }

@@ -51,16 +51,22 @@ struct Geo {
   static constexpr int FN = FACES * L;                                // face nodes per element
   static constexpr int FM = (FN + 31) / 32;                           // face nodes per lane
   static constexpr int HW = 2 * NV + 1;                               // trace: U[NV], F[NV], speed
-  static constexpr int WARPS = 8;                                     // warps per CTA
+  static constexpr int WARPS = 4;                                     // warps per CTA
   static constexpr int THREADS = 32 * WARPS;
-  // warp-private shared memory (doubles): fluxes [DIM][NV][NPE] | traces
-  // [face][HW][L] | face fluxes [face][NV][L]
+  static constexpr int MAXD = 4;                                      // max ring depth per warp
+  // shared memory: [mbarriers WARPS*MAXD][scratch RED] then per warp a slab
+  // (doubles): fluxes [DIM][NV][NPE] | traces [face][HW][L] | face fluxes
+  // [face][NV][L], followed by the warp's ring of D element slots, each
+  // holding u and the NU K_j of one element ([array][var][node], TMA-filled)
   static constexpr int OFF_T = DIM * NV * NPE;
   static constexpr int OFF_H = OFF_T + FACES * HW * L;
   static constexpr int WSLAB = ((OFF_H + FACES * NV * L) + 1) & ~1;
-  static constexpr int RED = 2 * WARPS;  // block reduction scratch (doubles)
-  static constexpr int SMEM = (WARPS * WSLAB + RED) * 8;
-  static constexpr bool MMA = (DIM == 2 && N == 8);  // FAST-mode tensor-core volume
+  static constexpr int RED = 2 * WARPS;                      // block reduction scratch (doubles)
+  static constexpr int HEAD = WARPS * MAXD + RED;            // 8-byte words before the slabs
+  static constexpr int CHUNK = NV * NPE;                     // one array of one element (doubles)
+  static constexpr bool TMA_OK = (CHUNK % 2) == 0;           // 16-byte element chunks
+  static constexpr bool MMA = (DIM == 2 && N == 8);          // FAST-mode tensor-core volume
+  static constexpr int smem_bytes(int nu, int depth) { return (HEAD + WARPS * (WSLAB + depth * (1 + nu) * CHUNK)) * 8; }
 
   // node index of position k along `axis` on transverse line t
   static __device__ __forceinline__ int node(int axis, int t, int k) {
@@ -89,16 +95,75 @@ struct Geo {
   }
 };
 
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* q) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(q));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+// the one arrival of a TMA-filled barrier, registering the bytes the copies complete
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                   smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+// Wait for the phase of parity `parity`.  A watchdog turns a lost completion
+// into a trapped kernel (a CUDA error) instead of a hung device.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  uint32_t polls = 0;
+  long long t0 = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (!done && (++polls & 4095u) == 0) {
+      if (t0 == 0) {
+        t0 = clock64();
+      } else if (clock64() - t0 > (1ll << 31)) {
+        printf("ndgx watchdog: block %d thread %d stuck on mbarrier %u (parity %u)\n", (int)blockIdx.x,
+               (int)threadIdx.x, smem_u32(b), parity);
+        __trap();
+      }
+    }
+  } while (!done);
+}
+// TMA bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 1/x to ~1 ulp for the contracted mode: the MUFU 64-bit reciprocal seed plus
+// two Newton steps (an IEEE division costs several times more).  Non-positive
+// x only occurs in a failing run (PhysicsError), where any value will do.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
 // D(8x8) += A(8x4, row) * B(4x8, col) in FP64 on the tensor cores
 __device__ __forceinline__ void dmma_8x8x4(double a, double b, double& c0, double& c1) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
 
 // U_s = u + sum_{t in amask} ca[t] ku[t] and (when `with_s`) S = u +
 // sum_{t in bmask} cb[t] ku[t], each in the reference's term order.
-template <bool EXACT, int NU>
+template <bool EXACT, int NU, int AM, int BM>
 __device__ __forceinline__ void combine_g(const StageArgs& p, size_t g, bool with_s, double& U, double& S) {
   using A = Ar<EXACT>;
   // issue every load first so they are all in flight together
@@ -109,25 +174,45 @@ __device__ __forceinline__ void combine_g(const StageArgs& p, size_t g, bool wit
   U = u;
 #pragma unroll
   for (int t = 0; t < NU; ++t)
-    if (p.amask >> t & 1) U = A::mac(U, p.ca[t], k[t]);
+    if ((AM >> t & 1) != 0) U = A::mac(U, p.ca[t], k[t]);
   S = u;
   if (with_s) {
 #pragma unroll
     for (int t = 0; t < NU; ++t)
-      if (p.bmask >> t & 1) S = A::mac(S, p.cb[t], k[t]);
+      if ((BM >> t & 1) != 0) S = A::mac(S, p.cb[t], k[t]);
+  }
+}
+
+// The same combination from an element slot in shared memory: array a at
+// src[a * stride] (0 = u, 1 + t = ku[t]).
+template <bool EXACT, int NU, int AM, int BM>
+__device__ __forceinline__ void combine_s(const StageArgs& p, const double* src, int stride, bool with_s, double& U,
+                                          double& S) {
+  using A = Ar<EXACT>;
+  const double u = src[0];
+  U = u;
+#pragma unroll
+  for (int t = 0; t < NU; ++t)
+    if ((AM >> t & 1) != 0) U = A::mac(U, p.ca[t], src[(1 + t) * stride]);
+  S = u;
+  if (with_s) {
+#pragma unroll
+    for (int t = 0; t < NU; ++t)
+      if ((BM >> t & 1) != 0) S = A::mac(S, p.cb[t], src[(1 + t) * stride]);
   }
 }
 
 // ============================================================ stage kernel
-// NU = p.nu, the number of K_j the stage reads (compile-time so that the
-// term loops unroll without predicates)
-template <int DIM, int N, int KIND, bool EXACT, int NU>
-__global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS, 2)
+// SIG indexes kSigs: the stage's term structure (p.nu, p.amask, p.bmask) at
+// compile time, so the term loops resolve without predicates
+template <int DIM, int N, int KIND, bool EXACT, int SIG>
+__global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS, 4)
 stage_kernel(const __grid_constant__ StageArgs p) {
   using G = Geo<DIM, N, KIND>;
   using A = Ar<EXACT>;
   constexpr int NV = G::NV, L = G::L, NPE = G::NPE, HW = G::HW;
   constexpr bool USE_MMA = G::MMA && !EXACT;
+  constexpr int NU = kSigs[SIG].nu, AM = kSigs[SIG].am, BM = kSigs[SIG].bm;
   extern __shared__ __align__(16) double smem[];
 
   Control* ctl = p.ctl;
@@ -142,11 +227,28 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   const double dt = p.rhs_only ? 1.0 : ctl->dt;
   const long long step = p.rhs_only ? 0 : ctl->steps;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double* sF = smem + wib * G::WSLAB;  // [DIM][NV][NPE]
-  double* sT = sF + G::OFF_T;          // [face][HW][L]
-  double* sH = sF + G::OFF_H;          // [face][NV][L]
+  constexpr int SLOT = (1 + NU) * G::CHUNK;  // one ring slot (doubles)
+  const int depth = G::TMA_OK ? p.depth : 0;  // 0: the node phase reads HBM directly
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + wib * G::MAXD;
+  double* sF = smem + G::HEAD + wib * (G::WSLAB + depth * SLOT);  // [DIM][NV][NPE]
+  double* sT = sF + G::OFF_T;                                     // [face][HW][L]
+  double* sH = sF + G::OFF_H;                                     // [face][NV][L]
+  double* ring = sF + G::WSLAB;                                   // [depth][1+NU][NV][NPE]
   const long long nwarps = (long long)gridDim.x * G::WARPS;
   double alpha = 0.0;
+  if (lane == 0)
+    for (int q = 0; q < depth; ++q) mbar_init(&bar[q], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  // lane 0 streams element ee's u and K_j into ring slot q with one bulk copy each
+  auto issue = [&](long long ee, int q) {
+    double* dst = ring + q * SLOT;
+    const size_t off = (size_t)ee * G::CHUNK;
+    mbar_arrive_expect_tx(&bar[q], (uint32_t)(SLOT * 8));
+    bulk_g2s(dst, p.u + off, G::CHUNK * 8, &bar[q]);
+#pragma unroll
+    for (int t = 0; t < NU; ++t) bulk_g2s(dst + (1 + t) * G::CHUNK, p.ku[t] + off, G::CHUNK * 8, &bar[q]);
+  };
 
   // MMA lane roles (2D N=8): lane = 4r + c
   const int r = lane >> 2, c = lane & 3;
@@ -165,8 +267,23 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   const int sx = nw % C0, sy = (nw / C0) % C1, sz = nw / (C0 * C1);
   int e = (int)blockIdx.x * G::WARPS + wib;
   int cx = e % C0, cy = (e / C0) % C1, cz = e / (C0 * C1);
+  if (lane == 0)
+    for (int q = 0; q + 1 < depth; ++q)
+      if (e + (long long)q * nw < nelem) issue(e + (long long)q * nw, q);
+  int slot = 0;
+  uint32_t parity = 0;
   for (; e < nelem; e += nw) {
     const size_t ebase = (size_t)e * NV * NPE;
+    const double* src = ring + slot * SLOT;  // this element's u and K_j (when depth > 0)
+    if (depth > 0) {
+      // keep depth-1 elements in flight: refill the slot the previous element used
+      const long long ahead = e + (long long)(depth - 1) * nw;
+      if (lane == 0 && ahead < nelem) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads first
+        issue(ahead, (slot + depth - 1) % depth);
+      }
+      mbar_wait(&bar[slot], parity);
+    }
     auto aos_cell = [&]() -> long long {  // global AoS cell index of this element
       const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
       return (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz;
@@ -184,7 +301,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         double S;
-        combine_g<EXACT, NU>(p, ebase + (size_t)v * NPE + n, last && !USE_MMA, U[v], S);
+        if (depth > 0)
+          combine_s<EXACT, NU, AM, BM>(p, src + v * NPE + n, G::CHUNK, last && !USE_MMA, U[v], S);
+        else
+          combine_g<EXACT, NU, AM, BM>(p, ebase + (size_t)v * NPE + n, last && !USE_MMA, U[v], S);
         Sn[m][v] = S;
       }
       if (KIND == 1 && !(U[0] > 0.0)) {
@@ -193,7 +313,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         const int nkey = (DIM == 2) ? j * N + i : (j * N + k) * N + i;
         record_error(ctl, error_key(step, p.phase, aos_cell(), nkey));
       }
-      const double rinv = (!EXACT && KIND == 1) ? 1.0 / U[0] : -1.0;
+      const double rinv = (!EXACT && KIND == 1) ? fast_rcp(U[0]) : -1.0;
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
         double F[NV], sp;
@@ -238,19 +358,19 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) Un[v] = __ldg(p.ext[d][side] + (xs * NV + v) * L + t);
       } else {
-        const int cw = side ? (ca + 1 == cn ? 0 : ca + 1) : (ca == 0 ? cn - 1 : ca - 1);
-        const size_t en = d == 0 ? (size_t)cw + (size_t)C0 * ((size_t)cy + (size_t)C1 * cz)
-                                 : (d == 1 ? (size_t)cx + (size_t)C0 * ((size_t)cw + (size_t)C1 * cz)
-                                           : (size_t)cx + (size_t)C0 * ((size_t)cy + (size_t)C1 * cw));
-        const size_t g = en * NV * NPE + G::node(d, t, side ? 0 : N - 1);
+        // neighbour element index: e -/+ stride_d, wrapped periodically
+        const int stride = d == 0 ? 1 : (d == 1 ? C0 : C0 * C1);
+        const int en = side ? (ca + 1 == cn ? e - (cn - 1) * stride : e + stride)
+                            : (ca == 0 ? e + (cn - 1) * stride : e - stride);
+        const size_t g = (size_t)en * (NV * NPE) + G::node(d, t, side ? 0 : N - 1);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           double S;
-          combine_g<EXACT, NU>(p, g + (size_t)v * NPE, false, Un[v], S);
+          combine_g<EXACT, NU, AM, BM>(p, g + (size_t)v * NPE, false, Un[v], S);
         }
       }
       double Fn[NV], sn;
-      flux<DIM, KIND, EXACT>(p, Un, d, Fn, sn);
+      flux<DIM, KIND, EXACT>(p, Un, d, Fn, sn, (!EXACT && KIND == 1) ? fast_rcp(Un[0]) : -1.0);
       const double so = own[2 * NV * L];
       const double a = dmax(side ? so : sn, side ? sn : so);
 #pragma unroll
@@ -266,6 +386,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     // ------------------------------------------------ 3: volume, faces, epilogue
     if constexpr (USE_MMA) {
       // outputs at nodes (i = r, j = 2c + s), all variables
+      const double xco = r == 0 ? p.lift[0] : (r == N - 1 ? -p.lift[0] : 0.0);
+      const int xf = r == N - 1 ? 1 : 0;
+      const double yco[2] = {c == 0 ? p.lift[1] : 0.0, c == 3 ? -p.lift[1] : 0.0};
+      const int yf[2] = {2, 3};
       double un[2][NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
@@ -279,20 +403,21 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
           const int j = 2 * c + s2;
-          // x faces at i = 0 / N-1 (line j), y faces at j = 0 / N-1 (line i = r)
-          if (r == 0) dv[s2] = fma(p.lift[0], sH[(0 * NV + v) * L + j], dv[s2]);
-          if (r == N - 1) dv[s2] = fma(-p.lift[0], sH[(1 * NV + v) * L + j], dv[s2]);
-          if (j == 0) dv[s2] = fma(p.lift[1], sH[(2 * NV + v) * L + r], dv[s2]);
-          if (j == N - 1) dv[s2] = fma(-p.lift[1], sH[(3 * NV + v) * L + r], dv[s2]);
+          // lifted face fluxes, branch-free: x faces at i = 0 / N-1 (line j),
+          // y faces at j = 0 / N-1 (line i = r); interior nodes add 0 * (a face value)
+          dv[s2] = fma(xco, sH[(xf * NV + v) * L + j], dv[s2]);
+          dv[s2] = fma(yco[s2], sH[(yf[s2] * NV + v) * L + r], dv[s2]);
           const size_t gi = ebase + (size_t)v * NPE + r + N * j;
           const double kv = dv[s2] * dt;
           if (!last) {
             p.out[gi] = kv;
           } else {
-            double S = __ldg(p.u + gi);
-#pragma unroll
-            for (int t = 0; t < NU; ++t)
-              if (p.bmask >> t & 1) S = fma(p.cb[t], __ldg(p.ku[t] + gi), S);
+            double S, Uu;
+            const int ln = v * NPE + r + N * j;
+            if (depth > 0)
+              combine_s<EXACT, NU, AM, BM>(p, src + ln, G::CHUNK, true, Uu, S);
+            else
+              combine_g<EXACT, NU, AM, BM>(p, ebase + ln, true, Uu, S);
             un[s2][v] = fma(p.b_last, kv, S);
             p.out[gi] = un[s2][v];
           }
@@ -301,10 +426,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       if (last) {
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
-          bool fin = true;
+          double sum = un[s2][0];  // non-finite iff some component is
 #pragma unroll
-          for (int v = 0; v < NV; ++v) fin = fin && isfinite(un[s2][v]);
-          if (!fin) record_error(ctl, error_key(step, kPhaseInstability, 0, 0));
+          for (int v = 1; v < NV; ++v) sum += un[s2][v];
+          if (!isfinite(sum)) record_error(ctl, error_key(step, kPhaseInstability, 0, 0));
           if (KIND == 1 && p.scan_alpha) {
             const int n = r + N * (2 * c + s2);
             if (!(un[s2][0] > 0.0)) {
@@ -313,7 +438,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
               double mm = 0.0;
 #pragma unroll
               for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[s2][1 + d]));
-              alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[s2][0]), p.sound_speed));
+              alpha = dmax(alpha, fma(mm, fast_rcp(un[s2][0]), p.sound_speed));  // contracted mode
             }
           }
         }
@@ -369,6 +494,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       }
     }
     __syncwarp();  // this element's slab reads precede the next element's writes
+    if (depth > 0 && ++slot == depth) {
+      slot = 0;
+      parity ^= 1;
+    }
     cx += sx;
     int carry = cx >= C0;
     cx -= carry ? C0 : 0;
@@ -381,7 +510,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   if (KIND == 1 && last && p.scan_alpha) {
     // block max of the non-negative wavespeeds on their IEEE bit patterns
     alpha = warp_max(alpha);
-    unsigned long long* red = reinterpret_cast<unsigned long long*>(smem + G::WARPS * G::WSLAB);
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(smem) + G::WARPS * G::MAXD;
     if (lane == 0) red[wib] = (unsigned long long)__double_as_longlong(alpha);
     __syncthreads();
     if (threadIdx.x == 0) {
