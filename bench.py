@@ -207,16 +207,32 @@ def bench_ours(args):
     dev = local
     dim, cells, order, eq, rk, desc = CONFIGS[args.config]
     arith = ndgx.ARITH_FAST if args.arith == "fast" else ndgx.ARITH_EXACT
-    mesh = ndgx.Mesh(dim, cells, order)
+    # weak scaling: every GPU owns the configuration's mesh; N GPUs stack N
+    # copies along the last axis (decompose() then gives slabs, one per rank)
+    gcells = list(cells)
+    gcells[dim - 1] *= world
+    mesh = ndgx.Mesh(dim, tuple(gcells), order)
     model = ndgx.EquationModel.isothermal_euler(dim, 1.0) if eq else ndgx.EquationModel.advection(dim, (1, 0, 0))
     cfg = ndgx.SolverConfig(mesh, model, rk, 0.4, 1.0)
-    dof = mesh.dof(model)
     stages = STAGES[rk]
 
-    # pinned host state (the reference AoS layout), synthetic IC
+    if world > 1:
+        # NCCL bootstrap over torch.distributed, then one ndgx rank per GPU
+        obj = [ndgx.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        s = ndgx.Solver.for_rank(cfg, world, rank, obj[0], device=dev, arith=arith)
+        lo, hi = tuple(s.plan.lo), tuple(s.plan.hi)
+    else:
+        s = ndgx.Solver(cfg, device=dev, arith=arith)
+        lo, hi = (0, 0, 0), tuple(mesh.cells)
+    dof = s.dof  # this rank's block
+
+    # pinned host state (the reference AoS layout), synthetic IC of this block
     host = torch.empty(dof, dtype=torch.float64, pin_memory=True)
     u0 = host.numpy()
-    if eq:
+    if world > 1:
+        ndgx.init_block(cfg, lo, hi, out=u0)
+    elif eq:
         ndgx.init_euler_subsonic(mesh, model, out=u0)
     else:
         ndgx.init_multisine(mesh, model, n_modes=40, seed=42, out=u0)
@@ -226,7 +242,6 @@ def bench_ours(args):
         if world > 1:
             dist.barrier()
 
-    s = ndgx.Solver(cfg, device=dev, arith=arith)
     s.upload_ptr(host.data_ptr())
     # warm-up: W untimed steps (graph capture, clocks)
     s.launch_steps(max(args.warmup, 3) if args.warmup >= 3 else 3)
@@ -284,7 +299,12 @@ def bench_ours(args):
     # ---- the bit-identical (reference operation order) mode, same workload ----
     exact = None
     if args.arith == "fast" and not args.no_exact_arm:
-        sx = ndgx.Solver(cfg, device=dev, arith=ndgx.ARITH_EXACT)
+        if world > 1:
+            obj = [ndgx.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            sx = ndgx.Solver.for_rank(cfg, world, rank, obj[0], device=dev, arith=ndgx.ARITH_EXACT)
+        else:
+            sx = ndgx.Solver(cfg, device=dev, arith=ndgx.ARITH_EXACT)
         sx.upload_ptr(host.data_ptr())
         sx.launch_steps(3)
         sx.sync()
@@ -293,8 +313,13 @@ def bench_ours(args):
         sx.launch_steps(args.steps)
         stx = sx.sync()
         barrier()
-        exact = {"value": world * dof * stages * args.steps / stx.wall_seconds, "unit": UNIT,
-                 "ms_per_step": stx.wall_seconds / args.steps * 1e3,
+        tx = stx.wall_seconds
+        if world > 1:
+            t = torch.tensor([tx], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tx = float(t.item())
+        exact = {"value": world * dof * stages * args.steps / tx, "unit": UNIT,
+                 "ms_per_step": tx / args.steps * 1e3,
                  "note": "arith=exact: the reference's IEEE operation order, states bit-identical to the CPU reference"}
         sx.close()
 
@@ -312,12 +337,13 @@ def bench_ours(args):
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (init_euler_subsonic IC of the reference, generated on the host)",
-            "config": {"workload": desc, "cells": list(cells), "order": order, "rk": RK_NAME[rk],
-                       "dof": dof, "arith": args.arith,
+            "config": {"workload": desc, "cells": list(cells), "global_cells": gcells, "order": order,
+                       "rk": RK_NAME[rk], "dof": dof, "dof_total": dof * world, "arith": args.arith,
                        "arith_note": ("fast = FP64 with FMA contraction and FP64 tensor-core (DMMA) volume "
                                       "quadrature, <= 1e-12 relative L2 vs the reference (tests/test_gpu_parity.py); "
                                       "exact = bit-identical") ,
-                       "parallelism": "dp1" if world == 1 else f"replicas x{world}",
+                       "parallelism": "1 GPU" if world == 1 else
+                       f"{world} ranks, decompose() blocks {list(s.plan.grid)}, NCCL face-halo exchange per RK stage",
                        "l2": "no flush needed: each state array (8*dof bytes) exceeds the 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

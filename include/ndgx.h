@@ -143,6 +143,42 @@ int ndgx_init_euler_subsonic(const ndgx_problem* p, double* u_aos);
 int ndgx_decompose(int dim, const int cells[3], int workers, int grid[3], int* lo, int* hi,
                    int* nbr, ndgx_error* err);
 
+/* ---------------------------------------------------------------- blocks
+ * Multi-GPU: one process per GPU, each owning one block of decompose()'s
+ * tiling of the global mesh (run_partitioned, src/partition.cpp:186-333,
+ * with its in-process Transport (include/ndg/transport.hpp:29-39) replaced by
+ * NCCL over NVLink).  Per RK stage each rank packs the stage-input face
+ * planes of its split axes, exchanges them with ncclSend/ncclRecv, and the
+ * stage kernel reads the received planes for its out-of-block faces; per
+ * step one ncclAllReduce(max) of the wavespeed bound (exchange_halos and the
+ * alpha barrier, src/partition.cpp:108-131, 236-261).  All of it is captured
+ * in the step CUDA graphs.  Results are identical to the single-block run. */
+typedef struct {
+  int rank, nranks;
+  int grid[3];           /* blocks per axis (decompose) */
+  int lo[3], hi[3];      /* this rank's global cell range [lo, hi) */
+  int split[3];          /* 1: faces along the axis come from the neighbour ranks */
+  int nbr[3][2];         /* neighbour rank [axis][low, high] */
+  long long plane[3];    /* doubles per face plane along the axis: cross-section cells * face nodes * vars */
+} ndgx_rank_plan;
+
+/* Block plan of `rank` (host only, no GPU).  force_exchange != 0 routes every
+ * axis through the transport, even a self-periodic one (test hook). */
+int ndgx_plan_rank(const ndgx_problem* global, int nranks, int rank, int force_exchange, ndgx_rank_plan* plan,
+                   ndgx_error* err);
+/* NCCL bootstrap: rank 0 creates the id, the caller broadcasts it (e.g. over
+ * torch.distributed), every rank passes it to ndgx_create_rank. */
+int ndgx_nccl_unique_id(unsigned char id[128], ndgx_error* err);
+/* A solver for this rank's block.  `global` describes the whole mesh; states
+ * exchanged with ndgx_upload/ndgx_download are the block's own AoS field. */
+int ndgx_create_rank(const ndgx_problem* global, int nranks, int rank, const unsigned char nccl_id[128],
+                     int force_exchange, ndgx_solver** out, ndgx_error* err);
+int ndgx_get_plan(const ndgx_solver* s, ndgx_rank_plan* plan);
+/* Initial conditions of the block [lo, hi) of the global mesh (block AoS). */
+int ndgx_init_multisine_block(const ndgx_problem* global, const double* amplitudes, int n_modes, const int lo[3],
+                              const int hi[3], double* u_aos);
+int ndgx_init_euler_subsonic_block(const ndgx_problem* global, const int lo[3], const int hi[3], double* u_aos);
+
 /* Library identification: "ndgx <version> sm_100a". */
 const char* ndgx_version(void);
 

@@ -29,7 +29,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=of
 # (source, object name, extra defines): the stage kernels are instantiated
 # once per (dim, order, arithmetic) so the objects compile in parallel
 SOURCES = [("ndgx_solver.cu", "ndgx_solver", []), ("ndgx_registry.cu", "ndgx_registry", []),
-           ("ndgx_setup.cpp", "ndgx_setup", [])] + [
+           ("ndgx_setup.cpp", "ndgx_setup", []), ("ndgx_nccl.cpp", "ndgx_nccl", [])] + [
     ("ndgx_inst.cu", f"ndgx_inst_d{d}_o{n}_e{e}",
      [f"-DNDGX_DIM={d}", f"-DNDGX_ORDER={n}", f"-DNDGX_EXACT={e}"])
     for d in (1, 2, 3) for n in range(2, 9) for e in (0, 1)]
@@ -52,7 +52,8 @@ def _compile(item) -> str:
         cmd = [NVCC] + ARCH + FLAGS + defs + ["-c", path, "-o", obj]
         if src.endswith(".cpp"):
             cxx = os.environ.get("CXX", shutil.which("g++") or "g++")
-            cmd = [cxx, "-O2", "-fPIC", "-ffp-contract=off", "-std=c++17", "-I", INCLUDE, "-I", CSRC,
+            cuda_inc = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(NVCC))), "include")
+            cmd = [cxx, "-O2", "-fPIC", "-ffp-contract=off", "-std=c++17", "-I", INCLUDE, "-I", CSRC, "-I", cuda_inc,
                    "-c", path, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -71,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         done = dict(zip([it[1] for it in order], ex.map(_compile, order)))
     objs = [done[it[1]] for it in SOURCES]
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lpthread"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -319,4 +319,69 @@ __global__ void permute_kernel(const double* __restrict__ src, double* __restric
   }
 }
 
+// ===================================================== face-plane packing
+// The stage-input traces of a block's boundary faces along its split axes,
+// for the neighbour ranks (pack_face_trace + exchange_halos, src/solver.cpp:
+// 166-187, src/partition.cpp:108-131): plane [d][side] holds U_s = u + sum
+// a K_j (the stage kernel's combination, same arithmetic) at the face nodes
+// of the cells with c_d = 0 (side 0) or C_d - 1 (side 1), laid out
+// [cross-section cell][var][face node] -- the layout StageArgs::ext reads.
+struct PackArgs {
+  const double* u;
+  const double* ku[kMaxTerms];
+  double ca[kMaxTerms];
+  int nu, amask;
+  int dim, order, nv, npe;
+  int cells[3];
+  int split[3];
+  long long plane[3];    // doubles per plane
+  double* snd[3][2];
+  Control* ctl;
+  int rhs_only;
+};
+
+template <bool EXACT>
+__global__ void pack_kernel(const __grid_constant__ PackArgs p) {
+  using A = Ar<EXACT>;
+  if (!p.rhs_only && (*(volatile int*)&p.ctl->skip || *(volatile unsigned long long*)&p.ctl->err_key != kNoError))
+    return;
+  const int N = p.order;
+  const int L = p.dim == 1 ? 1 : (p.dim == 2 ? N : N * N);
+  long long total = 0;
+  for (int d = 0; d < 3; ++d) total += p.split[d] ? 2 * p.plane[d] : 0;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    long long r = q;
+    int d = 0;
+    for (; d < 3; ++d) {
+      const long long sz = p.split[d] ? 2 * p.plane[d] : 0;
+      if (r < sz) break;
+      r -= sz;
+    }
+    const int side = (int)(r / p.plane[d]);
+    r -= side * p.plane[d];
+    const int t = (int)(r % L);
+    const long long xv = r / L;
+    const int v = (int)(xv % p.nv);
+    const long long xs = xv / p.nv;
+    // cross-section cell -> block cell
+    int c[3];
+    const int a1 = d == 0 ? 1 : 0, a2 = d == 2 ? 1 : 2;
+    c[a1] = (int)(xs % p.cells[a1]);
+    c[a2] = (int)(xs / p.cells[a1]);
+    c[d] = side ? p.cells[d] - 1 : 0;
+    const int k = side ? N - 1 : 0;
+    int n;  // node(d, t, k)
+    if (d == 0) n = k + N * t;
+    else if (d == 1) n = (t % N) + N * (k + N * (t / N));
+    else n = t + N * N * k;
+    const size_t e = (size_t)c[0] + (size_t)p.cells[0] * ((size_t)c[1] + (size_t)p.cells[1] * c[2]);
+    const size_t g = (e * p.nv + v) * p.npe + n;
+    double U = p.u[g];
+    for (int j = 0; j < p.nu; ++j)
+      if (p.amask >> j & 1) U = A::mac(U, p.ca[j], p.ku[j][g]);
+    p.snd[d][side][r] = U;
+  }
+}
+
 }  // namespace ndgx

@@ -190,6 +190,26 @@ double dt_numerator(const ndgx_problem* p) {
 
 using namespace ndgx;
 
+namespace ndgx {
+namespace {
+template <typename Fn>
+void for_each_block_node(const ndgx_problem* p, const int lo[3], const int hi[3], Fn&& fn) {
+  ndgx_problem local = *p;
+  for (int a = 0; a < 3; ++a) local.cells[a] = a < p->dim ? hi[a] - lo[a] : 1;
+  for_each_node_parallel(&local, [&](const int cell[3], const int node[3]) {
+    const int g[3] = {cell[0] + (p->dim > 0 ? lo[0] : 0), cell[1] + (p->dim > 1 ? lo[1] : 0),
+                      cell[2] + (p->dim > 2 ? lo[2] : 0)};
+    fn(&local, cell, g, node);
+  });
+}
+bool block_ok(const ndgx_problem* p, const int lo[3], const int hi[3]) {
+  for (int a = 0; a < p->dim; ++a)
+    if (lo[a] < 0 || hi[a] > p->cells[a] || lo[a] >= hi[a]) return false;
+  return true;
+}
+}  // namespace
+}  // namespace ndgx
+
 extern "C" {
 
 // gauss_lobatto (src/basis.cpp:32-76)
@@ -267,6 +287,49 @@ int ndgx_init_multisine(const ndgx_problem* p, const double* amps, int n_modes, 
     double v = 0.0;
     for (int k = 0; k < n_modes; ++k) v += amps[k] * std::sin(kTwoPi * static_cast<double>(k + 1) * x[0]);
     u[aos_index(p, 1, cell, node, 0)] = v;
+  });
+  return NDGX_OK;
+}
+
+// The same initial conditions restricted to the block [lo, hi) of the global
+// mesh `p`, written in the block's own AoS layout: every node value is the
+// global one (node coordinates come from the global cell index), so a
+// decomposed run starts from exactly the slices of the global field.
+
+int ndgx_init_multisine_block(const ndgx_problem* p, const double* amps, int n_modes, const int lo[3],
+                              const int hi[3], double* u) {
+  if (p->equation != NDGX_ADVECTION || n_modes < 1 || !block_ok(p, lo, hi)) return NDGX_ERR_CONFIG;
+  double gl[16], w[16];
+  if (ndgx_gauss_lobatto(p->order, gl, w)) return NDGX_ERR_CONFIG;
+  for_each_block_node(p, lo, hi, [&](const ndgx_problem* lp, const int cell[3], const int g[3], const int node[3]) {
+    double x[3];
+    node_coords(p, gl, g, node, x);
+    double v = 0.0;
+    for (int k = 0; k < n_modes; ++k) v += amps[k] * std::sin(kTwoPi * static_cast<double>(k + 1) * x[0]);
+    u[aos_index(lp, 1, cell, node, 0)] = v;
+  });
+  return NDGX_OK;
+}
+
+int ndgx_init_euler_subsonic_block(const ndgx_problem* p, const int lo[3], const int hi[3], double* u) {
+  if (p->equation != NDGX_EULER_ISOTHERMAL || p->dim < 2 || !block_ok(p, lo, hi)) return NDGX_ERR_CONFIG;
+  double gl[16], w[16];
+  if (ndgx_gauss_lobatto(p->order, gl, w)) return NDGX_ERR_CONFIG;
+  const int nv = p->dim + 1;
+  const double a = p->sound_speed;
+  for_each_block_node(p, lo, hi, [&](const ndgx_problem* lp, const int cell[3], const int g[3], const int node[3]) {
+    double x[3];
+    node_coords(p, gl, g, node, x);
+    const double sx = std::sin(kTwoPi * x[0]);
+    const double sy = std::sin(kTwoPi * x[1]);
+    double rho = 1.0 + 0.2 * sx * sy;
+    if (p->dim == 3) rho = 1.0 + 0.2 * sx * sy * std::sin(kTwoPi * x[2]);
+    const double ux = 0.5 * a * sy;
+    const double uy = 0.5 * a * sx;
+    u[aos_index(lp, nv, cell, node, 0)] = rho;
+    u[aos_index(lp, nv, cell, node, 1)] = rho * ux;
+    u[aos_index(lp, nv, cell, node, 2)] = rho * uy;
+    if (p->dim == 3) u[aos_index(lp, nv, cell, node, 3)] = 0.0;
   });
   return NDGX_OK;
 }

@@ -19,6 +19,7 @@
 
 #include "ndgx.h"
 #include "ndgx_kernels.h"
+#include "ndgx_nccl.h"
 #include "ndgx_setup.h"
 
 using ndgx::Control;
@@ -46,6 +47,10 @@ void clear_error(ndgx_error* e) {
   e->worker = -1;
   e->cell[0] = e->cell[1] = e->cell[2] = -1;
 }
+
+struct TransportFailure {
+  std::string what;
+};
 
 struct CudaFailure {
   cudaError_t rc;
@@ -86,6 +91,15 @@ struct ndgx_solver {
   long long graph_fixed = -2;
   double graph_tend = -1.0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // block of a decomposed mesh (defaults: the whole mesh, no exchange)
+  ndgx_rank_plan plan{};
+  int gcells[3] = {1, 1, 1};
+  int goff[3] = {0, 0, 0};
+  bool exchange = false;            // some axis takes its halo from the transport
+  ncclComm_t comm = nullptr;
+  const ndgx::Nccl* nc = nullptr;
+  double* snd[3][2] = {};           // packed boundary planes (ours)
+  double* rcv[3][2] = {};           // received planes (neighbours')
   long long pending_fixed = -1;  // ndgx_launch_steps bookkeeping
   int pending_start_parity = 0;
 
@@ -134,8 +148,9 @@ struct ndgx_solver {
     s.scan_alpha = (s.is_last && kind == NDGX_EULER_ISOTHERMAL) ? 1 : 0;
     for (int d = 0; d < 3; ++d) {
       s.cells[d] = cells[d];
-      s.gcells[d] = cells[d];
-      s.goff[d] = 0;
+      s.gcells[d] = gcells[d];
+      s.goff[d] = goff[d];
+      for (int q = 0; q < 2; ++q) s.ext[d][q] = plan.split[d] ? rcv[d][q] : nullptr;
       s.vel[d] = p.velocity[d];
       s.lift[d] = lift[d];
       for (int q = 0; q < 64; ++q) s.K[d][q] = K[d][q];
@@ -146,7 +161,68 @@ struct ndgx_solver {
     return s;
   }
 
+  // Per stage: pack our boundary planes, swap them with the neighbours
+  // (exchange_halos, src/partition.cpp:108-131: per axis send the high plane
+  // up and receive the low halo, send the low plane down and receive the
+  // high halo -- the same posting order on every rank, so pairs match even
+  // when both neighbours are one rank or this rank itself).
+  void launch_exchange(const StageArgs& s) const {
+    ndgx::PackArgs pa;
+    std::memset(&pa, 0, sizeof(pa));
+    pa.u = s.u;
+    for (int t = 0; t < ndgx::kMaxTerms; ++t) {
+      pa.ku[t] = s.ku[t];
+      pa.ca[t] = s.ca[t];
+    }
+    pa.nu = s.nu;
+    pa.amask = s.amask;
+    pa.dim = dim;
+    pa.order = N;
+    pa.nv = nv;
+    pa.npe = npe;
+    pa.ctl = s.ctl;
+    pa.rhs_only = s.rhs_only;
+    long long total = 0;
+    for (int d = 0; d < 3; ++d) {
+      pa.cells[d] = cells[d];
+      pa.split[d] = plan.split[d];
+      pa.plane[d] = plan.plane[d];
+      pa.snd[d][0] = snd[d][0];
+      pa.snd[d][1] = snd[d][1];
+      if (plan.split[d]) total += 2 * plan.plane[d];
+    }
+    const int threads = 256;
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((total + threads - 1) / threads, 148LL * 8));
+    if (exact)
+      ndgx::pack_kernel<true><<<blocks, threads, 0, stream>>>(pa);
+    else
+      ndgx::pack_kernel<false><<<blocks, threads, 0, stream>>>(pa);
+    nccl_check(nc->GroupStart(), "ncclGroupStart");
+    for (int d = 0; d < dim; ++d) {
+      if (!plan.split[d]) continue;
+      const size_t n = (size_t)plan.plane[d];
+      nccl_check(nc->Send(snd[d][1], n, ncclFloat64, plan.nbr[d][1], comm, stream), "ncclSend");
+      nccl_check(nc->Recv(rcv[d][0], n, ncclFloat64, plan.nbr[d][0], comm, stream), "ncclRecv");
+      nccl_check(nc->Send(snd[d][0], n, ncclFloat64, plan.nbr[d][0], comm, stream), "ncclSend");
+      nccl_check(nc->Recv(rcv[d][1], n, ncclFloat64, plan.nbr[d][1], comm, stream), "ncclRecv");
+    }
+    nccl_check(nc->GroupEnd(), "ncclGroupEnd");
+  }
+
+  // Per step: every rank's dt comes from the global max wavespeed (the
+  // alpha barrier of run_partitioned, src/partition.cpp:201-213, 243-252).
+  void launch_alpha_reduce(Control* c) const {
+    if (!comm || kind != NDGX_EULER_ISOTHERMAL) return;
+    nccl_check(nc->AllReduce(&c->alpha_bits, &c->alpha_bits, 1, ncclUint64, ncclMax, comm, stream),
+               "ncclAllReduce");
+  }
+
+  void nccl_check(ncclResult_t r, const char* what) const {
+    if (r != ncclSuccess) throw TransportFailure{std::string(what) + ": " + nc->GetErrorString(r)};
+  }
+
   void launch_stage(const StageArgs& s) const {
+    if (exchange) launch_exchange(s);
     // persistent CTAs (one element per warp): as many as are co-resident
     const long long warps = (long long)cells[0] * cells[1] * cells[2];
     const long long need = (warps + kern.warps - 1) / kern.warps;
@@ -168,6 +244,7 @@ struct ndgx_solver {
   }
 
   void launch_step(const StepParams& sp, int par, Control* c) const {
+    launch_alpha_reduce(c);
     ndgx::step_begin_kernel<<<1, 1, 0, stream>>>(sp);
     for (int i = 0; i < stages; ++i) launch_stage(stage_args(i, par, c, false));
   }
@@ -209,7 +286,8 @@ struct ndgx_solver {
     const StepParams sp = step_params(ctl, fixed, 0);
     for (int par = 0; par < 2; ++par) {
       cudaGraph_t g;
-      ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+      ck(cudaStreamBeginCapture(stream, comm ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal),
+         "begin capture");
       launch_step(sp, par, ctl);
       launch_step(sp, 1 - par, ctl);
       ck(cudaStreamEndCapture(stream, &g), "end capture");
@@ -279,11 +357,19 @@ struct ndgx_solver {
   }
 
   // device index of (AoS cell index, AoS node key, var)
+  // block-local cell of a global AoS cell index (the kernels name cells globally)
+  void local_cell(long long aos_cell, int c[3]) const {
+    const int g2 = gcells[2], g1 = gcells[1];
+    c[2] = (int)(aos_cell % g2) - goff[2];
+    c[1] = (int)((aos_cell / g2) % g1) - goff[1];
+    c[0] = (int)(aos_cell / ((long long)g2 * g1)) - goff[0];
+  }
+
   size_t device_index(long long aos_cell, int aos_node, int var) const {
-    const int c2 = cells[2], c1 = cells[1];
-    const int cz = (int)(aos_cell % c2);
-    const int cy = (int)((aos_cell / c2) % c1);
-    const int cx = (int)(aos_cell / ((long long)c2 * c1));
+    const int c1 = cells[1];
+    int lc[3];
+    local_cell(aos_cell, lc);
+    const int cx = lc[0], cy = lc[1], cz = lc[2];
     int i = 0, j = 0, k = 0;
     if (dim == 1) i = aos_node;
     if (dim == 2) { i = aos_node / N; j = aos_node % N; }
@@ -330,9 +416,7 @@ struct ndgx_solver {
       rho += a[stage][j] * fetch(k_buf(j, par), idx);
     }
     int c[3];
-    c[2] = (int)(cell % cells[2]);
-    c[1] = (int)((cell / cells[2]) % cells[1]);
-    c[0] = (int)(cell / ((long long)cells[2] * cells[1]));
+    local_cell(cell, c);
     const std::string where = "(" + std::to_string(c[0]) + "," + std::to_string(c[1]) + "," +
                               std::to_string(c[2]) + ")";
     set_error(err, NDGX_ERR_PHYSICS,
@@ -342,6 +426,21 @@ struct ndgx_solver {
   }
 
   ~ndgx_solver() {
+    // graphs that captured NCCL work go before the communicator; the
+    // communicator is torn down with ncclCommAbort (ncclCommDestroy can block
+    // on the proxy of a communicator whose graphs were captured)
+    for (auto& g : graph)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+    if (stream) cudaStreamSynchronize(stream);
+    if (comm && nc) nc->CommAbort(comm);
+    for (int d = 0; d < 3; ++d)
+      for (int q = 0; q < 2; ++q) {
+        if (snd[d][q]) cudaFree(snd[d][q]);
+        if (rcv[d][q]) cudaFree(rcv[d][q]);
+      }
     for (auto& g : graph)
       if (g) cudaGraphExecDestroy(g);
     for (double* q : buf) cudaFree(q);
@@ -393,11 +492,22 @@ int validate_problem(const ndgx_problem* p, ndgx_error* err) {
 
 }  // namespace
 
+static int create_block(const ndgx_problem* prob, const ndgx_rank_plan* plan, ndgx_solver** out, ndgx_error* err);
+
 extern "C" {
 
 const char* ndgx_version(void) { return "ndgx 0.1.0 sm_100a"; }
 
 int ndgx_create(const ndgx_problem* prob, ndgx_solver** out, ndgx_error* err) {
+  return create_block(prob, nullptr, out, err);
+}
+
+}  // extern "C"
+
+// A solver for `plan`'s block of the global mesh `prob` (nullptr: the whole
+// mesh).  The operator, dt numerator and wavespeed use the global mesh, so
+// every block computes with the reference's exact coefficients.
+static int create_block(const ndgx_problem* prob, const ndgx_rank_plan* plan, ndgx_solver** out, ndgx_error* err) {
   clear_error(err);
   if (!prob || !out) {
     set_error(err, NDGX_ERR_CONFIG, "null argument");
@@ -432,7 +542,21 @@ int ndgx_create(const ndgx_problem* prob, ndgx_solver** out, ndgx_error* err) {
     s->kind = prob->equation;
     s->nv = s->kind == NDGX_ADVECTION ? 1 : s->dim + 1;
     s->exact = prob->arith != NDGX_ARITH_FAST;
-    for (int a = 0; a < 3; ++a) s->cells[a] = a < s->dim ? prob->cells[a] : 1;
+    for (int a = 0; a < 3; ++a) {
+      s->gcells[a] = a < s->dim ? prob->cells[a] : 1;
+      s->goff[a] = plan ? plan->lo[a] : 0;
+      s->cells[a] = plan ? plan->hi[a] - plan->lo[a] : s->gcells[a];
+    }
+    if (plan) {
+      s->plan = *plan;
+      for (int a = 0; a < 3; ++a) s->exchange = s->exchange || plan->split[a] != 0;
+    } else {
+      s->plan.nranks = 1;
+      for (int a = 0; a < 3; ++a) {
+        s->plan.grid[a] = 1;
+        s->plan.hi[a] = s->cells[a];
+      }
+    }
     s->npe = 1;
     for (int a = 0; a < s->dim; ++a) s->npe *= s->N;
     s->n = (size_t)s->nv * s->npe * s->cells[0] * s->cells[1] * s->cells[2];
@@ -491,12 +615,110 @@ int ndgx_create(const ndgx_problem* prob, ndgx_solver** out, ndgx_error* err) {
     ck(cudaMalloc(&s->ctl, sizeof(Control)), "cudaMalloc control");
     ck(cudaMalloc(&s->ctl_warm, sizeof(Control)), "cudaMalloc control");
     ck(cudaMallocHost(&s->h_ctl, sizeof(Control)), "cudaMallocHost");
+    for (int d = 0; d < 3; ++d)
+      if (s->plan.split[d])
+        for (int q = 0; q < 2; ++q) {
+          ck(cudaMalloc(&s->snd[d][q], s->plan.plane[d] * sizeof(double)), "cudaMalloc plane");
+          ck(cudaMalloc(&s->rcv[d][q], s->plan.plane[d] * sizeof(double)), "cudaMalloc plane");
+          ck(cudaMemsetAsync(s->rcv[d][q], 0, s->plan.plane[d] * sizeof(double), s->stream), "memset");
+        }
     ck(cudaStreamSynchronize(s->stream), "sync");
   } catch (const CudaFailure& f) {
     delete s;
     return cuda_error(err, f);
   }
   *out = s;
+  return NDGX_OK;
+}
+
+extern "C" {
+
+int ndgx_plan_rank(const ndgx_problem* global, int nranks, int rank, int force_exchange, ndgx_rank_plan* plan,
+                   ndgx_error* err) {
+  clear_error(err);
+  if (!global || !plan) {
+    set_error(err, NDGX_ERR_CONFIG, "null argument");
+    return NDGX_ERR_CONFIG;
+  }
+  if (int rc = validate_problem(global, err)) return rc;
+  if (nranks < 1 || rank < 0 || rank >= nranks) {
+    set_error(err, NDGX_ERR_CONFIG, "rank " + std::to_string(rank) + " outside 0.." + std::to_string(nranks - 1));
+    return NDGX_ERR_CONFIG;
+  }
+  std::vector<int> lo(3 * nranks), hi(3 * nranks), nbr(6 * nranks);
+  ndgx_rank_plan pl;
+  std::memset(&pl, 0, sizeof(pl));
+  if (int rc = ndgx_decompose(global->dim, global->cells, nranks, pl.grid, lo.data(), hi.data(), nbr.data(), err))
+    return rc;
+  pl.rank = rank;
+  pl.nranks = nranks;
+  const int nv = global->equation == NDGX_ADVECTION ? 1 : global->dim + 1;
+  const int N = global->order;
+  const long long L = global->dim == 1 ? 1 : (global->dim == 2 ? N : (long long)N * N);
+  for (int a = 0; a < 3; ++a) {
+    pl.lo[a] = lo[3 * rank + a];
+    pl.hi[a] = hi[3 * rank + a];
+    pl.nbr[a][0] = nbr[6 * rank + 2 * a];
+    pl.nbr[a][1] = nbr[6 * rank + 2 * a + 1];
+    pl.split[a] = a < global->dim && (pl.grid[a] > 1 || force_exchange) ? 1 : 0;
+  }
+  for (int a = 0; a < 3; ++a) {
+    long long cross = 1;
+    for (int b = 0; b < 3; ++b)
+      if (b != a) cross *= pl.hi[b] - pl.lo[b];
+    pl.plane[a] = a < global->dim ? cross * L * nv : 0;
+  }
+  *plan = pl;
+  return NDGX_OK;
+}
+
+int ndgx_nccl_unique_id(unsigned char id[128], ndgx_error* err) {
+  clear_error(err);
+  std::string why;
+  const ndgx::Nccl* nc = ndgx::nccl(&why);
+  if (!nc) {
+    set_error(err, NDGX_ERR_TRANSPORT, why);
+    return NDGX_ERR_TRANSPORT;
+  }
+  ncclUniqueId uid;
+  const ncclResult_t r = nc->GetUniqueId(&uid);
+  if (r != ncclSuccess) {
+    set_error(err, NDGX_ERR_TRANSPORT, std::string("ncclGetUniqueId: ") + nc->GetErrorString(r));
+    return NDGX_ERR_TRANSPORT;
+  }
+  std::memcpy(id, uid.internal, sizeof(uid.internal));
+  return NDGX_OK;
+}
+
+int ndgx_create_rank(const ndgx_problem* global, int nranks, int rank, const unsigned char nccl_id[128],
+                     int force_exchange, ndgx_solver** out, ndgx_error* err) {
+  ndgx_rank_plan plan;
+  if (int rc = ndgx_plan_rank(global, nranks, rank, force_exchange, &plan, err)) return rc;
+  std::string why;
+  const ndgx::Nccl* nc = ndgx::nccl(&why);
+  if (!nc) {
+    set_error(err, NDGX_ERR_TRANSPORT, why);
+    return NDGX_ERR_TRANSPORT;
+  }
+  if (int rc = create_block(global, &plan, out, err)) return rc;
+  ndgx_solver* s = *out;
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, nccl_id, sizeof(uid.internal));
+  cudaSetDevice(global->device);
+  const ncclResult_t r = nc->CommInitRank(&s->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    ndgx_destroy(s);
+    *out = nullptr;
+    set_error(err, NDGX_ERR_TRANSPORT, std::string("ncclCommInitRank: ") + nc->GetErrorString(r));
+    return NDGX_ERR_TRANSPORT;
+  }
+  s->nc = nc;
+  return NDGX_OK;
+}
+
+int ndgx_get_plan(const ndgx_solver* s, ndgx_rank_plan* plan) {
+  if (!s || !plan) return NDGX_ERR_CONFIG;
+  *plan = s->plan;
   return NDGX_OK;
 }
 
@@ -535,6 +757,9 @@ int ndgx_upload(ndgx_solver* s, const double* u_aos, ndgx_error* err) {
     ck(cudaStreamSynchronize(s->stream), "upload sync");
   } catch (const CudaFailure& f) {
     return cuda_error(err, f);
+  } catch (const TransportFailure& t) {
+    set_error(err, NDGX_ERR_TRANSPORT, t.what);
+    return NDGX_ERR_TRANSPORT;
   }
   return NDGX_OK;
 }
@@ -550,6 +775,9 @@ int ndgx_download(ndgx_solver* s, double* u_aos, ndgx_error* err) {
     ck(cudaStreamSynchronize(s->stream), "download sync");
   } catch (const CudaFailure& f) {
     return cuda_error(err, f);
+  } catch (const TransportFailure& t) {
+    set_error(err, NDGX_ERR_TRANSPORT, t.what);
+    return NDGX_ERR_TRANSPORT;
   }
   return NDGX_OK;
 }
@@ -570,6 +798,9 @@ int ndgx_rhs(ndgx_solver* s, double* dudt_aos, ndgx_error* err) {
     ck(cudaStreamSynchronize(s->stream), "rhs sync");
   } catch (const CudaFailure& f) {
     return cuda_error(err, f);
+  } catch (const TransportFailure& t) {
+    set_error(err, NDGX_ERR_TRANSPORT, t.what);
+    return NDGX_ERR_TRANSPORT;
   }
   return NDGX_OK;
 }
@@ -660,6 +891,9 @@ int ndgx_advance(ndgx_solver* s, long fixed_steps, int warmup, ndgx_stats* stats
     return finish_run(s, fixed, start_par, stats, err);
   } catch (const CudaFailure& f) {
     return cuda_error(err, f);
+  } catch (const TransportFailure& t) {
+    set_error(err, NDGX_ERR_TRANSPORT, t.what);
+    return NDGX_ERR_TRANSPORT;
   }
 }
 
@@ -677,6 +911,9 @@ int ndgx_launch_steps(ndgx_solver* s, long steps, ndgx_error* err) {
     for (long long q = 0; q < (fixed + 1) / 2; ++q) ck(cudaGraphLaunch(s->graph[s->parity], s->stream), "graph");
   } catch (const CudaFailure& f) {
     return cuda_error(err, f);
+  } catch (const TransportFailure& t) {
+    set_error(err, NDGX_ERR_TRANSPORT, t.what);
+    return NDGX_ERR_TRANSPORT;
   }
   return NDGX_OK;
 }
@@ -694,6 +931,9 @@ int ndgx_sync(ndgx_solver* s, ndgx_stats* stats, ndgx_error* err) {
     return finish_run(s, fixed, s->pending_start_parity, stats, err);
   } catch (const CudaFailure& f) {
     return cuda_error(err, f);
+  } catch (const TransportFailure& t) {
+    set_error(err, NDGX_ERR_TRANSPORT, t.what);
+    return NDGX_ERR_TRANSPORT;
   }
 }
 
@@ -718,6 +958,9 @@ int ndgx_profile_step(ndgx_solver* s, float* ms, int n, ndgx_error* err) {
     for (auto& e : ev) cudaEventDestroy(e);
   } catch (const CudaFailure& f) {
     return cuda_error(err, f);
+  } catch (const TransportFailure& t) {
+    set_error(err, NDGX_ERR_TRANSPORT, t.what);
+    return NDGX_ERR_TRANSPORT;
   }
   return NDGX_OK;
 }

@@ -94,6 +94,16 @@ class Error(C.Structure):
                 ("cell", C.c_int * 3), ("message", C.c_char * 256)]
 
 
+class RankPlan(C.Structure):
+    """ndgx_rank_plan: one rank's block of decompose()'s tiling (include/ndgx.h)."""
+    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("grid", C.c_int * 3), ("lo", C.c_int * 3),
+                ("hi", C.c_int * 3), ("split", C.c_int * 3), ("nbr", (C.c_int * 2) * 3),
+                ("plane", C.c_longlong * 3)]
+
+    def cells(self):
+        return tuple(self.hi[a] - self.lo[a] for a in range(3))
+
+
 _lib = None
 
 
@@ -134,6 +144,12 @@ def lib() -> C.CDLL:
     L.ndgx_decompose.argtypes = [C.c_int, P(C.c_int), C.c_int, P(C.c_int), P(C.c_int), P(C.c_int),
                                  P(C.c_int), P(Error)]
     L.ndgx_version.restype = C.c_char_p
+    L.ndgx_plan_rank.argtypes = [P(Problem), C.c_int, C.c_int, C.c_int, P(RankPlan), P(Error)]
+    L.ndgx_nccl_unique_id.argtypes = [C.c_char_p, P(Error)]
+    L.ndgx_create_rank.argtypes = [P(Problem), C.c_int, C.c_int, C.c_char_p, C.c_int, P(C.c_void_p), P(Error)]
+    L.ndgx_get_plan.argtypes = [C.c_void_p, P(RankPlan)]
+    L.ndgx_init_multisine_block.argtypes = [P(Problem), D, C.c_int, P(C.c_int), P(C.c_int), D]
+    L.ndgx_init_euler_subsonic_block.argtypes = [P(Problem), P(C.c_int), P(C.c_int), D]
     _lib = L
     return L
 
@@ -309,16 +325,34 @@ def make_problem(config: SolverConfig, device: int = 0, arith: int = ARITH_EXACT
 class Solver:
     """A device-resident solver handle (one ndgx_solver)."""
 
-    def __init__(self, config: SolverConfig, device: int = 0, arith: int = ARITH_EXACT, basis=None):
+    def __init__(self, config: SolverConfig, device: int = 0, arith: int = ARITH_EXACT, basis=None,
+                 _rank=None):
         validate(config)
         self.config = config
         self.problem = make_problem(config, device, arith, basis)
         self._h = C.c_void_p()
         err = Error()
-        _check(lib().ndgx_create(C.byref(self.problem), C.byref(self._h), C.byref(err)), err)
+        if _rank is None:
+            _check(lib().ndgx_create(C.byref(self.problem), C.byref(self._h), C.byref(err)), err)
+        else:
+            nranks, rank, nccl_id, force = _rank
+            _check(lib().ndgx_create_rank(C.byref(self.problem), nranks, rank, nccl_id, int(force),
+                                          C.byref(self._h), C.byref(err)), err)
         self.size = int(lib().ndgx_state_size(self._h))
         self.dof = int(lib().ndgx_dof(self._h))
         self.stages = int(lib().ndgx_stages(self._h))
+        self.plan = RankPlan()
+        lib().ndgx_get_plan(self._h, C.byref(self.plan))
+
+    @classmethod
+    def for_rank(cls, config: SolverConfig, nranks: int, rank: int, nccl_id: bytes, device: int = 0,
+                 arith: int = ARITH_EXACT, force_exchange: bool = False) -> "Solver":
+        """This rank's block of `config.mesh` (the GLOBAL mesh), exchanging face
+        halos over NCCL with the other ranks (run_partitioned, src/partition.cpp:186-333)."""
+        if len(nccl_id) != 128:
+            raise TransportError("an NCCL unique id is 128 bytes")
+        _preload_nccl()
+        return cls(config, device, arith, None, _rank=(nranks, rank, nccl_id, force_exchange))
 
     def close(self):
         if self._h:
@@ -491,6 +525,66 @@ def decompose(mesh: Mesh, worker_count: int) -> BlockDecomposition:
         blocks.append(Block(coord, tuple(lo[3 * k:3 * k + 3]), tuple(hi[3 * k:3 * k + 3]),
                             tuple((nbr[6 * k + 2 * a], nbr[6 * k + 2 * a + 1]) for a in range(3))))
     return BlockDecomposition(worker_count, g, blocks)
+
+
+def plan_rank(config: SolverConfig, nranks: int, rank: int, force_exchange: bool = False) -> RankPlan:
+    """The block of `rank` in decompose()'s tiling of the global mesh (no GPU needed)."""
+    p = make_problem(config)
+    plan, err = RankPlan(), Error()
+    _check(lib().ndgx_plan_rank(C.byref(p), nranks, rank, int(force_exchange), C.byref(plan), C.byref(err)), err)
+    return plan
+
+
+_nccl_preloaded = False
+
+
+def _preload_nccl() -> None:
+    """Make libndgx's dlopen("libnccl.so.2") resolve to PyTorch's bundled NCCL
+    (the one torch.distributed already uses in the same process), not a
+    second, older system copy."""
+    global _nccl_preloaded
+    if _nccl_preloaded:
+        return
+    _nccl_preloaded = True
+    try:
+        import nvidia.nccl  # the wheel torch links against
+        path = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            C.CDLL(path, mode=C.RTLD_GLOBAL)
+    except Exception:  # noqa: BLE001 -- fall back to the system libnccl.so.2
+        pass
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 creates it; broadcast it to every rank)."""
+    _preload_nccl()
+    buf = C.create_string_buffer(128)
+    err = Error()
+    _check(lib().ndgx_nccl_unique_id(buf, C.byref(err)), err)
+    return buf.raw
+
+
+def init_block(config: SolverConfig, lo, hi, n_modes: int = 40, seed: int = 42,
+               out: Optional[np.ndarray] = None) -> np.ndarray:
+    """The reference's initial condition (init_euler_subsonic for Euler,
+    init_multisine otherwise) on the block [lo, hi) of the global mesh, in the
+    block's own AoS layout -- exactly the slice of the global field."""
+    p = make_problem(config)
+    lo3 = (C.c_int * 3)(*(list(lo) + [0, 0, 0])[:3])
+    hi3 = (C.c_int * 3)(*(list(hi) + [1, 1, 1])[:3])
+    n = config.model.n_var() * config.mesh.nodes_per_cell()
+    for a in range(config.mesh.dim):
+        n *= hi3[a] - lo3[a]
+    if out is None:
+        out = np.zeros(n)
+    if config.model.kind == EULER_ISOTHERMAL:
+        rc = lib().ndgx_init_euler_subsonic_block(C.byref(p), lo3, hi3, _dptr(out))
+    else:
+        amps = multisine_amplitudes(n_modes, seed)
+        rc = lib().ndgx_init_multisine_block(C.byref(p), _dptr(amps), len(amps), lo3, hi3, _dptr(out))
+    if rc != 0:
+        raise ConfigError("init_block: invalid block or model")
+    return out
 
 
 def version() -> str:
