@@ -43,7 +43,7 @@ StageKernel make_stage_kernel() {
   k.threads = G::THREADS;
   k.warps = G::WARPS;
   k.smem_fixed = G::smem_bytes(0, 0);
-  k.ring_per_array = G::WARPS * G::CHUNK * 8;
+  k.ring_per_array = G::WARPS * G::SLOT1 * 8;
   k.tma_ok = G::TMA_OK;
   return k;
 }

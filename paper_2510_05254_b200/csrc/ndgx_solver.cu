@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <new>
@@ -325,6 +326,9 @@ struct ndgx_solver {
         return NDGX_ERR_CONFIG;
       }
     }
+    // NDGX_DEPTH=<d> forces one ring depth (0 = direct loads) where it fits (tuning)
+    const char* env = std::getenv("NDGX_DEPTH");
+    const int forced = env ? std::atoi(env) : -1;
     for (int q = 0; q < ndgx::kNumSigs; ++q) {
       const int nu = ndgx::kSigs[q].nu;
       const void* fn = reinterpret_cast<const void*>(kern.fn[q]);
@@ -332,6 +336,7 @@ struct ndgx_solver {
       long long best_score = -1;
       for (int d = kern.tma_ok ? 4 : 0; d >= 0; --d) {
         if (d == 1) continue;  // a ring needs one slot ahead
+        if (forced >= 0 && d != forced && !(d == 0 && !kern.tma_ok)) continue;
         const int bytes = kern.smem(nu, d);
         if (bytes > limit) continue;
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attribute");

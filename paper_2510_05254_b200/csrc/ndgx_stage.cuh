@@ -66,7 +66,11 @@ struct Geo {
   static constexpr int CHUNK = NV * NPE;                     // one array of one element (doubles)
   static constexpr bool TMA_OK = (CHUNK % 2) == 0;           // 16-byte element chunks
   static constexpr bool MMA = (DIM == 2 && N == 8);          // FAST-mode tensor-core volume
-  static constexpr int smem_bytes(int nu, int depth) { return (HEAD + WARPS * (WSLAB + depth * (1 + nu) * CHUNK)) * 8; }
+  // one face node per lane: the ring slot also carries the element's face
+  // neighbour values ([array][var][lane], cp.async), so no load is on demand
+  static constexpr bool FACE_PF = (FM == 1);
+  static constexpr int SLOT1 = CHUNK + (FACE_PF ? 32 * NV : 0);  // ring doubles per input array
+  static constexpr int smem_bytes(int nu, int depth) { return (HEAD + WARPS * (WSLAB + depth * (1 + nu) * SLOT1)) * 8; }
 
   // node index of position k along `axis` on transverse line t
   static __device__ __forceinline__ int node(int axis, int t, int k) {
@@ -154,6 +158,15 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(y, e, y);
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(PENDING) : "memory");
+}
+
 // D(8x8) += A(8x4, row) * B(4x8, col) in FP64 on the tensor cores
 __device__ __forceinline__ void dmma_8x8x4(double a, double b, double& c0, double& c1) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -202,10 +215,220 @@ __device__ __forceinline__ void combine_s(const StageArgs& p, const double* src,
   }
 }
 
+// ------------------------------------------------------------ flagship body
+// One element of the 2D, N = 8, contracted-arithmetic stage (the benchmark
+// shape), written for issue efficiency: lane constants are hoisted by the
+// caller (Lane8), global accesses use per-element base pointers with
+// immediate offsets, and the only branches are warp-uniform.
+struct Lane8 {
+  int r, c;              // lane = 4r + c
+  int n0;                // flux node h = 0: (i = c, j = r); h = 1 is n0 + 4
+  int f, t;              // face lane: face f (x-lo, x-hi, y-lo, y-hi), face node t
+  int nb_node;           // the neighbour element's node facing this face lane
+  int o0;                // output node s = 0: (i = r, j = 2c); s = 1 is o0 + 8
+  double xco, yco0, yco1;  // face-lift coefficients of the output nodes
+  int xf;                // x face (0 / 1) feeding the output row r
+  double kx[2], ky[2];   // K_x[r][c+4h], K_y[r][c+4h]
+};
+
+template <int KIND, int NU, int AM, int BM>
+__device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8& ln, int lane, int e, int cx,
+                                                 int cy, const double* src, const double* fsrc, bool ring,
+                                                 double* sF, double* sT, double* sH, double dt, bool last,
+                                                 long long step, double& alpha) {
+  constexpr int N = 8, NPE = 64, L = 8;
+  constexpr int NV = KIND == 0 ? 1 : 3;
+  constexpr int HW = 2 * NV + 1;
+  constexpr int CHUNK = NV * NPE;
+  using A = Ar<false>;
+  const int C0 = p.cells[0], C1 = p.cells[1];
+  const size_t ebase = (size_t)e * CHUNK;
+  const double a2 = KIND == 1 ? p.sound_speed : 0.0;
+
+  // ---------------------------------------------------------- nodes
+  double Bx[2][NV];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int n = ln.n0 + 4 * h;
+    double U[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double S;
+      if (ring) combine_s<false, NU, AM, BM>(p, src + v * NPE + n, CHUNK, false, U[v], S);
+      else combine_g<false, NU, AM, BM>(p, ebase + v * NPE + n, false, U[v], S);
+    }
+    double Fx[NV], Fy[NV], sx, sy;
+    if (KIND == 0) {
+      Fx[0] = p.vel[0] * U[0];
+      Fy[0] = p.vel[1] * U[0];
+      sx = fabs(p.vel[0]);
+      sy = fabs(p.vel[1]);
+    } else {
+      if (!(U[0] > 0.0)) {
+        const int i = n & 7, j = n >> 3;
+        const long long gx = cx + p.goff[0], gy = cy + p.goff[1];
+        record_error(p.ctl, error_key(step, p.phase, (gx * p.gcells[1] + gy) * (long long)p.gcells[2], j * N + i));
+      }
+      const double rinv = fast_rcp(U[0]);
+      const double ux = U[1] * rinv, uy = U[2] * rinv;
+      const double pr = U[0] * a2 * a2;  // (rho a) a
+      Fx[0] = U[1];
+      Fx[1] = fma(ux, U[1], pr);
+      Fx[2] = ux * U[2];
+      Fy[0] = U[2];
+      Fy[1] = uy * U[1];
+      Fy[2] = fma(uy, U[2], pr);
+      sx = fabs(ux) + a2;
+      sy = fabs(uy) + a2;
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      Bx[h][v] = Fx[v];
+      sF[v * NPE + n] = Fy[v];
+    }
+    // face traces: x faces at i = c + 4h = 0 / 7, y faces at j = r = 0 / 7
+    const int i = ln.c + 4 * h;
+    if (i == 0 || i == N - 1) {
+      double* t = sT + (i == 0 ? 0 : HW) * L + ln.r;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        t[v * L] = U[v];
+        t[(NV + v) * L] = Fx[v];
+      }
+      t[2 * NV * L] = sx;
+    }
+    if (ln.r == 0 || ln.r == N - 1) {
+      double* t = sT + ((ln.r == 0 ? 2 : 3) * HW) * L + i;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        t[v * L] = U[v];
+        t[(NV + v) * L] = Fy[v];
+      }
+      t[2 * NV * L] = sy;
+    }
+  }
+  __syncwarp();
+
+  // ---------------------------------------------------------- faces
+  {
+    const int f = ln.f, d = f >> 1, side = f & 1;
+    const bool bnd = d == 0 ? (side ? cx == C0 - 1 : cx == 0) : (side ? cy == C1 - 1 : cy == 0);
+    const double* ext = p.ext[d][side];
+    double Un[NV];
+    if (bnd && ext != nullptr) {
+      const size_t xs = d == 0 ? (size_t)cy : (size_t)cx;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Un[v] = ring ? fsrc[v * 32 + lane] : __ldg(ext + (xs * NV + v) * L + ln.t);
+    } else if (ring) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double S;
+        combine_s<false, NU, AM, BM>(p, fsrc + v * 32 + lane, NV * 32, false, Un[v], S);
+      }
+    } else {
+      const int step_d = d == 0 ? 1 : C0;
+      const int span = d == 0 ? C0 : C1;
+      const int en = side ? (bnd ? e - (span - 1) * step_d : e + step_d) : (bnd ? e + (span - 1) * step_d : e - step_d);
+      const size_t g = (size_t)en * CHUNK + ln.nb_node;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double S;
+        combine_g<false, NU, AM, BM>(p, g + v * NPE, false, Un[v], S);
+      }
+    }
+    double Fn[NV], sn;
+    if (KIND == 0) {
+      Fn[0] = p.vel[d] * Un[0];
+      sn = fabs(p.vel[d]);
+    } else {
+      const double rinv = fast_rcp(Un[0]);
+      const double ua = Un[1 + d] * rinv;
+      const double pr = Un[0] * a2 * a2;
+      Fn[0] = Un[1 + d];
+      Fn[1] = d == 0 ? fma(ua, Un[1], pr) : ua * Un[1];
+      Fn[2] = d == 0 ? ua * Un[2] : fma(ua, Un[2], pr);
+      sn = fabs(ua) + a2;
+    }
+    const double* own = sT + (f * HW) * L + ln.t;
+    const double so = own[2 * NV * L];
+    const double al = dmax(so, sn);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
+      const double uo = own[v * L], fo = own[(NV + v) * L];
+      const double um = side ? uo : Un[v], up = side ? Un[v] : uo;
+      const double fm = side ? fo : Fn[v], fp = side ? Fn[v] : fo;
+      sH[(f * NV + v) * L + ln.t] = 0.5 * ((fm + fp) - al * (up - um));
+    }
+  }
+  __syncwarp();
+
+  // ---------------------------------------------------------- volume + epilogue
+  double* gout = p.out + ebase;
+  double un[2][NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double d0 = 0.0, d1 = 0.0;
+    dmma_8x8x4(ln.kx[0], Bx[0][v], d0, d1);  // D_x = K_x F_x
+    dmma_8x8x4(ln.kx[1], Bx[1][v], d0, d1);
+    const double* Fy = sF + v * NPE;
+    dmma_8x8x4(Fy[ln.r + N * ln.c], ln.ky[0], d0, d1);  // += F_y K_y^T
+    dmma_8x8x4(Fy[ln.r + N * (ln.c + 4)], ln.ky[1], d0, d1);
+    // lifted face fluxes: x faces on rows r = 0 / 7 (line j), y faces on
+    // columns j = 0 (s = 0 of c = 0) / 7 (s = 1 of c = 3) (line i = r)
+    const double* hx = sH + (ln.xf * NV + v) * L + 2 * ln.c;
+    d0 = fma(ln.xco, hx[0], d0);
+    d1 = fma(ln.xco, hx[1], d1);
+    d0 = fma(ln.yco0, sH[(2 * NV + v) * L + ln.r], d0);
+    d1 = fma(ln.yco1, sH[(3 * NV + v) * L + ln.r], d1);
+    const double k0 = d0 * dt, k1 = d1 * dt;
+    if (!last) {
+      gout[v * NPE + ln.o0] = k0;
+      gout[v * NPE + ln.o0 + 8] = k1;
+    } else {
+      double S0, S1, U0, U1;
+      if (ring) {
+        combine_s<false, NU, AM, BM>(p, src + v * NPE + ln.o0, CHUNK, true, U0, S0);
+        combine_s<false, NU, AM, BM>(p, src + v * NPE + ln.o0 + 8, CHUNK, true, U1, S1);
+      } else {
+        combine_g<false, NU, AM, BM>(p, ebase + v * NPE + ln.o0, true, U0, S0);
+        combine_g<false, NU, AM, BM>(p, ebase + v * NPE + ln.o0 + 8, true, U1, S1);
+      }
+      un[0][v] = fma(p.b_last, k0, S0);
+      un[1][v] = fma(p.b_last, k1, S1);
+      gout[v * NPE + ln.o0] = un[0][v];
+      gout[v * NPE + ln.o0 + 8] = un[1][v];
+    }
+  }
+  if (last) {
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      double sum = un[s2][0];  // non-finite iff some component is
+#pragma unroll
+      for (int v = 1; v < NV; ++v) sum += un[s2][v];
+      if (!isfinite(sum)) record_error(p.ctl, error_key(step, kPhaseInstability, 0, 0));
+      if (KIND == 1 && p.scan_alpha) {
+        if (!(un[s2][0] > 0.0)) {
+          const int n = ln.o0 + 8 * s2;
+          const long long gx = cx + p.goff[0], gy = cy + p.goff[1];
+          record_error(p.ctl, error_key(step + 1, kPhaseScan, (gx * p.gcells[1] + gy) * (long long)p.gcells[2],
+                                        (n & 7) * N + (n >> 3)));
+        } else {
+          const double mm = dmax(fabs(un[s2][1]), fabs(un[s2][2]));
+          alpha = dmax(alpha, fma(mm, fast_rcp(un[s2][0]), p.sound_speed));
+        }
+      }
+    }
+  }
+  __syncwarp();  // this element's slab reads precede the next element's writes
+}
+
 // ============================================================ stage kernel
 // SIG indexes kSigs: the stage's term structure (p.nu, p.amask, p.bmask) at
 // compile time, so the term loops resolve without predicates
 template <int DIM, int N, int KIND, bool EXACT, int SIG>
+// <= 128 registers (4 CTAs = 16 warps per SM): capping at 80 for 24 warps
+// measured 25% slower (less load-level parallelism per warp)
 __global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS, 4)
 stage_kernel(const __grid_constant__ StageArgs p) {
   using G = Geo<DIM, N, KIND>;
@@ -227,7 +450,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   const double dt = p.rhs_only ? 1.0 : ctl->dt;
   const long long step = p.rhs_only ? 0 : ctl->steps;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  constexpr int SLOT = (1 + NU) * G::CHUNK;  // one ring slot (doubles)
+  constexpr int SLOT = (1 + NU) * G::SLOT1;  // one ring slot (doubles): arrays | face neighbour values
   const int depth = G::TMA_OK ? p.depth : 0;  // 0: the node phase reads HBM directly
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + wib * G::MAXD;
   double* sF = smem + G::HEAD + wib * (G::WSLAB + depth * SLOT);  // [DIM][NV][NPE]
@@ -241,17 +464,69 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncwarp();
   // lane 0 streams element ee's u and K_j into ring slot q with one bulk copy each
-  auto issue = [&](long long ee, int q) {
+  // element ee = (ex, ey, ez): lane 0 streams its u and K_j into ring slot q
+  // with one bulk copy each; with FACE_PF every face lane also copies its
+  // neighbour face node (or the received plane) with cp.async (one group)
+  auto issue = [&](int ee, int ex, int ey, int ez, int q) {
     double* dst = ring + q * SLOT;
     const size_t off = (size_t)ee * G::CHUNK;
-    mbar_arrive_expect_tx(&bar[q], (uint32_t)(SLOT * 8));
-    bulk_g2s(dst, p.u + off, G::CHUNK * 8, &bar[q]);
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bar[q], (uint32_t)((1 + NU) * G::CHUNK * 8));
+      bulk_g2s(dst, p.u + off, G::CHUNK * 8, &bar[q]);
 #pragma unroll
-    for (int t = 0; t < NU; ++t) bulk_g2s(dst + (1 + t) * G::CHUNK, p.ku[t] + off, G::CHUNK * 8, &bar[q]);
+      for (int t = 0; t < NU; ++t) bulk_g2s(dst + (1 + t) * G::CHUNK, p.ku[t] + off, G::CHUNK * 8, &bar[q]);
+    }
+    if constexpr (G::FACE_PF) {
+      double* fr = dst + (1 + NU) * G::CHUNK;  // [array][var][lane]
+      if (lane < G::FN) {
+        const int f = lane / L, t = lane - f * L;
+        const int d = f >> 1, side = f & 1;
+        const int ca = d == 0 ? ex : (d == 1 ? ey : ez);
+        const int cn = d == 0 ? C0 : (d == 1 ? C1 : C2);
+        const bool boundary = side ? (ca == cn - 1) : (ca == 0);
+        if (boundary && p.ext[d][side] != nullptr) {
+          const size_t xs = d == 0 ? (size_t)ey + (size_t)C1 * ez
+                                   : (d == 1 ? (size_t)ex + (size_t)C0 * ez : (size_t)ex + (size_t)C0 * ey);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) cp_async8(fr + v * 32 + lane, p.ext[d][side] + (xs * NV + v) * L + t);
+        } else {
+          const int stride = d == 0 ? 1 : (d == 1 ? C0 : C0 * C1);
+          const int en = side ? (ca + 1 == cn ? ee - (cn - 1) * stride : ee + stride)
+                              : (ca == 0 ? ee + (cn - 1) * stride : ee - stride);
+          const size_t g = (size_t)en * (NV * NPE) + G::node(d, t, side ? 0 : N - 1);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            cp_async8(fr + v * 32 + lane, p.u + g + (size_t)v * NPE);
+#pragma unroll
+            for (int a = 0; a < NU; ++a) cp_async8(fr + ((1 + a) * NV + v) * 32 + lane, p.ku[a] + g + (size_t)v * NPE);
+          }
+        }
+      }
+      cp_async_commit();
+    }
   };
 
   // MMA lane roles (2D N=8): lane = 4r + c
   const int r = lane >> 2, c = lane & 3;
+  Lane8 ln8{};
+  if constexpr (USE_MMA) {
+    ln8.r = r;
+    ln8.c = c;
+    ln8.n0 = c + N * r;
+    ln8.f = lane >> 3;
+    ln8.t = lane & 7;
+    // the neighbour's facing node: x-lo (7, t), x-hi (0, t), y-lo (t, 7), y-hi (t, 0)
+    ln8.nb_node = ln8.f == 0 ? 7 + 8 * ln8.t : (ln8.f == 1 ? 8 * ln8.t : (ln8.f == 2 ? ln8.t + 56 : ln8.t));
+    ln8.o0 = r + 16 * c;
+    ln8.xco = r == 0 ? p.lift[0] : (r == N - 1 ? -p.lift[0] : 0.0);
+    ln8.xf = r == N - 1 ? 1 : 0;
+    ln8.yco0 = c == 0 ? p.lift[1] : 0.0;
+    ln8.yco1 = c == 3 ? -p.lift[1] : 0.0;
+    for (int h = 0; h < 2; ++h) {
+      ln8.kx[h] = p.K[0][r * N + c + 4 * h];
+      ln8.ky[h] = p.K[1][r * N + c + 4 * h];
+    }
+  }
   double kx[2] = {0.0, 0.0}, ky[2] = {0.0, 0.0};
   if constexpr (USE_MMA) {
 #pragma unroll
@@ -267,22 +542,56 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   const int sx = nw % C0, sy = (nw / C0) % C1, sz = nw / (C0 * C1);
   int e = (int)blockIdx.x * G::WARPS + wib;
   int cx = e % C0, cy = (e / C0) % C1, cz = e / (C0 * C1);
-  if (lane == 0)
-    for (int q = 0; q + 1 < depth; ++q)
-      if (e + (long long)q * nw < nelem) issue(e + (long long)q * nw, q);
+  auto step_coords = [&](int& x, int& y, int& z) {
+    x += sx;
+    int carry = x >= C0;
+    x -= carry ? C0 : 0;
+    y += sy + carry;
+    carry = y >= C1;
+    y -= carry ? C1 : 0;
+    z += sz + carry;
+  };
+  // the element `depth - 1` iterations ahead (the next one to issue)
+  int ae = e, ax = cx, ay = cy, az = cz;
+  for (int q = 0; q + 1 < depth; ++q) {
+    if (ae < nelem) issue(ae, ax, ay, az, q);
+    else if (G::FACE_PF) cp_async_commit();  // keep one group per slot
+    ae += nw;
+    step_coords(ax, ay, az);
+  }
   int slot = 0;
   uint32_t parity = 0;
   for (; e < nelem; e += nw) {
     const size_t ebase = (size_t)e * NV * NPE;
     const double* src = ring + slot * SLOT;  // this element's u and K_j (when depth > 0)
+    const double* fsrc = src + (1 + NU) * G::CHUNK;  // its face neighbour values (FACE_PF)
     if (depth > 0) {
       // keep depth-1 elements in flight: refill the slot the previous element used
-      const long long ahead = e + (long long)(depth - 1) * nw;
-      if (lane == 0 && ahead < nelem) {
+      if (ae < nelem) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads first
-        issue(ahead, (slot + depth - 1) % depth);
+        issue(ae, ax, ay, az, (slot + depth - 1) % depth);
+      } else if (G::FACE_PF) {
+        cp_async_commit();
       }
+      ae += nw;
+      step_coords(ax, ay, az);
       mbar_wait(&bar[slot], parity);
+      if constexpr (G::FACE_PF) {
+        // this element's group is the oldest of the depth in flight
+        if (depth == 2) cp_async_wait<1>();
+        else if (depth == 3) cp_async_wait<2>();
+        else cp_async_wait<3>();
+      }
+    }
+    if constexpr (USE_MMA) {
+      element_2d8_fast<KIND, NU, AM, BM>(p, ln8, lane, e, cx, cy, src, fsrc, depth > 0, sF, sT, sH, dt, last, step,
+                                         alpha);
+      if (depth > 0 && ++slot == depth) {
+        slot = 0;
+        parity ^= 1;
+      }
+      step_coords(cx, cy, cz);
+      continue;
     }
     auto aos_cell = [&]() -> long long {  // global AoS cell index of this element
       const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
@@ -352,7 +661,15 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       const int cn = d == 0 ? C0 : (d == 1 ? C1 : C2);
       const bool boundary = side ? (ca == cn - 1) : (ca == 0);
       double Un[NV];
-      if (boundary && p.ext[d][side] != nullptr) {
+      if (G::FACE_PF && depth > 0) {
+        const bool ext = boundary && p.ext[d][side] != nullptr;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double S;
+          if (ext) Un[v] = fsrc[v * 32 + lane];
+          else combine_s<EXACT, NU, AM, BM>(p, fsrc + v * 32 + lane, NV * 32, false, Un[v], S);
+        }
+      } else if (boundary && p.ext[d][side] != nullptr) {
         const size_t xs = d == 0 ? (size_t)cy + (size_t)C1 * cz
                                  : (d == 1 ? (size_t)cx + (size_t)C0 * cz : (size_t)cx + (size_t)C0 * cy);
 #pragma unroll
@@ -498,14 +815,9 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       slot = 0;
       parity ^= 1;
     }
-    cx += sx;
-    int carry = cx >= C0;
-    cx -= carry ? C0 : 0;
-    cy += sy + carry;
-    carry = cy >= C1;
-    cy -= carry ? C1 : 0;
-    cz += sz + carry;
+    step_coords(cx, cy, cz);
   }
+  if constexpr (G::FACE_PF) cp_async_wait<0>();  // no copy outlives the kernel
 
   if (KIND == 1 && last && p.scan_alpha) {
     // block max of the non-negative wavespeeds on their IEEE bit patterns

@@ -3,7 +3,7 @@ sys.path.insert(0, ".")
 import numpy as np
 import paper_2510_05254_b200 as ndgx
 out = {}
-for arith in (ndgx.ARITH_EXACT, ndgx.ARITH_FAST):
+for arith in ([int(a) for a in sys.argv[1].split(",")] if len(sys.argv) > 1 else (ndgx.ARITH_EXACT, ndgx.ARITH_FAST)):
     for (dim, cells, order, eq, rk) in [(2,(768,768),8,1,ndgx.RK4), (3,(128,128,128),4,1,ndgx.RK6), (2,(388,388),8,0,ndgx.RK4)]:
         mesh = ndgx.Mesh(dim, cells, order)
         model = ndgx.EquationModel.isothermal_euler(dim,1.0) if eq else ndgx.EquationModel.advection(dim,(1,0,0))
