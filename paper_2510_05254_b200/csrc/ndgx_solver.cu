@@ -321,7 +321,8 @@ struct ndgx_solver {
         if (ub) t.bmask |= 1 << t.nu;
         ++t.nu;
       }
-      if (sig_of(t) < 0) {
+      // the kernels take "last stage" from the signature (b-terms present)
+      if (sig_of(t) < 0 || (i == stages - 1) != (t.bmask != 0)) {
         set_error(err, NDGX_ERR_CONFIG, "Runge-Kutta tableau without a compiled stage signature");
         return NDGX_ERR_CONFIG;
       }
@@ -334,7 +335,7 @@ struct ndgx_solver {
       const void* fn = reinterpret_cast<const void*>(kern.fn[q]);
       ndgx::StageLaunch best;
       long long best_score = -1;
-      for (int d = kern.tma_ok ? 4 : 0; d >= 0; --d) {
+      for (int d = (kern.tma_ok && (!kern.prefer_direct || forced > 0)) ? 4 : 0; d >= 0; --d) {
         if (d == 1) continue;  // a ring needs one slot ahead
         if (forced >= 0 && d != forced && !(d == 0 && !kern.tma_ok)) continue;
         const int bytes = kern.smem(nu, d);

@@ -70,7 +70,13 @@ struct Geo {
   // neighbour values ([array][var][lane], cp.async), so no load is on demand
   static constexpr bool FACE_PF = (FM == 1);
   static constexpr int SLOT1 = CHUNK + (FACE_PF ? 32 * NV : 0);  // ring doubles per input array
-  static constexpr int smem_bytes(int nu, int depth) { return (HEAD + WARPS * (WSLAB + depth * (1 + nu) * SLOT1)) * 8; }
+  // the tensor-core body stages only F_y (F_x stays in registers as MMA fragments)
+  static constexpr __host__ __device__ int wslab(bool mma) {
+    return mma ? (((2 * NV * NPE + FACES * HW * L + FACES * NV * L) + 1) & ~1) : WSLAB;
+  }
+  static constexpr int smem_bytes(int nu, int depth, bool mma) {
+    return (HEAD + WARPS * (wslab(mma) + depth * (1 + nu) * SLOT1)) * 8;
+  }
 
   // node index of position k along `axis` on transverse line t
   static __device__ __forceinline__ int node(int axis, int t, int k) {
@@ -215,6 +221,43 @@ __device__ __forceinline__ void combine_s(const StageArgs& p, const double* src,
   }
 }
 
+// U_s at two adjacent nodes (16-byte aligned) of one variable, from the ring
+// slot (`ring`) or HBM: one 16-byte load per input array.
+template <int NU, int AM, int BM = 0>
+__device__ __forceinline__ void combine_pair(const StageArgs& p, bool ring, const double* s, size_t g, int stride,
+                                             double& U0, double& U1, double* S0 = nullptr, double* S1 = nullptr) {
+  double2 k[NU > 0 ? NU : 1];
+  double2 u;
+  if (ring) {
+    u = *reinterpret_cast<const double2*>(s);
+#pragma unroll
+    for (int t = 0; t < NU; ++t) k[t] = *reinterpret_cast<const double2*>(s + (1 + t) * stride);
+  } else {
+    u = __ldg(reinterpret_cast<const double2*>(p.u + g));
+#pragma unroll
+    for (int t = 0; t < NU; ++t) k[t] = __ldg(reinterpret_cast<const double2*>(p.ku[t] + g));
+  }
+  U0 = u.x;
+  U1 = u.y;
+#pragma unroll
+  for (int t = 0; t < NU; ++t)
+    if ((AM >> t & 1) != 0) {
+      U0 = fma(p.ca[t], k[t].x, U0);
+      U1 = fma(p.ca[t], k[t].y, U1);
+    }
+  if (S0 != nullptr) {  // last stage: S = u + sum b_j K_j from the same loads
+    double a = u.x, b = u.y;
+#pragma unroll
+    for (int t = 0; t < NU; ++t)
+      if ((BM >> t & 1) != 0) {
+        a = fma(p.cb[t], k[t].x, a);
+        b = fma(p.cb[t], k[t].y, b);
+      }
+    *S0 = a;
+    *S1 = b;
+  }
+}
+
 // ------------------------------------------------------------ flagship body
 // One element of the 2D, N = 8, contracted-arithmetic stage (the benchmark
 // shape), written for issue efficiency: lane constants are hoisted by the
@@ -222,13 +265,13 @@ __device__ __forceinline__ void combine_s(const StageArgs& p, const double* src,
 // immediate offsets, and the only branches are warp-uniform.
 struct Lane8 {
   int r, c;              // lane = 4r + c
-  int n0;                // flux node h = 0: (i = c, j = r); h = 1 is n0 + 4
+  int n0;                // flux nodes (i = 2c + h, j = r): n0 and n0 + 1 (adjacent)
   int f, t;              // face lane: face f (x-lo, x-hi, y-lo, y-hi), face node t
   int nb_node;           // the neighbour element's node facing this face lane
   int o0;                // output node s = 0: (i = r, j = 2c); s = 1 is o0 + 8
   double xco, yco0, yco1;  // face-lift coefficients of the output nodes
   int xf;                // x face (0 / 1) feeding the output row r
-  double kx[2], ky[2];   // K_x[r][c+4h], K_y[r][c+4h]
+  double kx[2], ky[2];   // K_x[r][2c+h], K_y[r][2c+h] (k-step h pairs l = 2c + h)
 };
 
 template <int KIND, int NU, int AM, int BM>
@@ -246,17 +289,27 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   const double a2 = KIND == 1 ? p.sound_speed : 0.0;
 
   // ---------------------------------------------------------- nodes
-  double Bx[2][NV];
+  double Bx[2][NV], Fyp[2][NV];
+  // both nodes of the lane at once: one 16-byte load per (array, var)
+  double Up[2][NV];
+  double* sS = sF + NV * NPE;  // last stage: S at the flux nodes, read back at the output nodes
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (last) {
+      double S0, S1;
+      combine_pair<NU, AM, BM>(p, ring, src + v * NPE + ln.n0, ebase + v * NPE + ln.n0, CHUNK, Up[0][v], Up[1][v],
+                               &S0, &S1);
+      *reinterpret_cast<double2*>(sS + v * NPE + ln.n0) = make_double2(S0, S1);
+    } else {
+      combine_pair<NU, AM>(p, ring, src + v * NPE + ln.n0, ebase + v * NPE + ln.n0, CHUNK, Up[0][v], Up[1][v]);
+    }
+  }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int n = ln.n0 + 4 * h;
+    const int n = ln.n0 + h;
     double U[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      double S;
-      if (ring) combine_s<false, NU, AM, BM>(p, src + v * NPE + n, CHUNK, false, U[v], S);
-      else combine_g<false, NU, AM, BM>(p, ebase + v * NPE + n, false, U[v], S);
-    }
+    for (int v = 0; v < NV; ++v) U[v] = Up[h][v];
     double Fx[NV], Fy[NV], sx, sy;
     if (KIND == 0) {
       Fx[0] = p.vel[0] * U[0];
@@ -284,10 +337,10 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       Bx[h][v] = Fx[v];
-      sF[v * NPE + n] = Fy[v];
+      Fyp[h][v] = Fy[v];
     }
-    // face traces: x faces at i = c + 4h = 0 / 7, y faces at j = r = 0 / 7
-    const int i = ln.c + 4 * h;
+    // face traces: x faces at i = 2c + h = 0 / 7, y faces at j = r = 0 / 7
+    const int i = 2 * ln.c + h;
     if (i == 0 || i == N - 1) {
       double* t = sT + (i == 0 ? 0 : HW) * L + ln.r;
 #pragma unroll
@@ -307,6 +360,9 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       t[2 * NV * L] = sy;
     }
   }
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+    *reinterpret_cast<double2*>(sF + v * NPE + ln.n0) = make_double2(Fyp[0][v], Fyp[1][v]);
   __syncwarp();
 
   // ---------------------------------------------------------- faces
@@ -372,8 +428,8 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
     dmma_8x8x4(ln.kx[0], Bx[0][v], d0, d1);  // D_x = K_x F_x
     dmma_8x8x4(ln.kx[1], Bx[1][v], d0, d1);
     const double* Fy = sF + v * NPE;
-    dmma_8x8x4(Fy[ln.r + N * ln.c], ln.ky[0], d0, d1);  // += F_y K_y^T
-    dmma_8x8x4(Fy[ln.r + N * (ln.c + 4)], ln.ky[1], d0, d1);
+    dmma_8x8x4(Fy[ln.r + N * (2 * ln.c)], ln.ky[0], d0, d1);  // += F_y K_y^T, A = F_y[i=r][j=2c+h]
+    dmma_8x8x4(Fy[ln.r + N * (2 * ln.c + 1)], ln.ky[1], d0, d1);
     // lifted face fluxes: x faces on rows r = 0 / 7 (line j), y faces on
     // columns j = 0 (s = 0 of c = 0) / 7 (s = 1 of c = 3) (line i = r)
     const double* hx = sH + (ln.xf * NV + v) * L + 2 * ln.c;
@@ -386,14 +442,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       gout[v * NPE + ln.o0] = k0;
       gout[v * NPE + ln.o0 + 8] = k1;
     } else {
-      double S0, S1, U0, U1;
-      if (ring) {
-        combine_s<false, NU, AM, BM>(p, src + v * NPE + ln.o0, CHUNK, true, U0, S0);
-        combine_s<false, NU, AM, BM>(p, src + v * NPE + ln.o0 + 8, CHUNK, true, U1, S1);
-      } else {
-        combine_g<false, NU, AM, BM>(p, ebase + v * NPE + ln.o0, true, U0, S0);
-        combine_g<false, NU, AM, BM>(p, ebase + v * NPE + ln.o0 + 8, true, U1, S1);
-      }
+      const double S0 = sS[v * NPE + ln.o0], S1 = sS[v * NPE + ln.o0 + 8];
       un[0][v] = fma(p.b_last, k0, S0);
       un[1][v] = fma(p.b_last, k1, S1);
       gout[v * NPE + ln.o0] = un[0][v];
@@ -446,17 +495,21 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 
   const int C0 = p.cells[0], C1 = p.cells[1], C2 = p.cells[2];
   const long long nelem = (long long)C0 * C1 * C2;
-  const bool last = p.is_last != 0;
+  // the last stage is exactly the signature with b-terms (kSigs), so the
+  // epilogue variant is resolved at compile time
+  constexpr bool last = kSigs[SIG].bm != 0;
   const double dt = p.rhs_only ? 1.0 : ctl->dt;
   const long long step = p.rhs_only ? 0 : ctl->steps;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   constexpr int SLOT = (1 + NU) * G::SLOT1;  // one ring slot (doubles): arrays | face neighbour values
   const int depth = G::TMA_OK ? p.depth : 0;  // 0: the node phase reads HBM directly
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + wib * G::MAXD;
-  double* sF = smem + G::HEAD + wib * (G::WSLAB + depth * SLOT);  // [DIM][NV][NPE]
-  double* sT = sF + G::OFF_T;                                     // [face][HW][L]
-  double* sH = sF + G::OFF_H;                                     // [face][NV][L]
-  double* ring = sF + G::WSLAB;                                   // [depth][1+NU][NV][NPE]
+  constexpr int WSL = G::wslab(USE_MMA);
+  constexpr int OFFT = USE_MMA ? 2 * NV * NPE : G::OFF_T;  // MMA: F_y | S
+  double* sF = smem + G::HEAD + wib * (WSL + depth * SLOT);  // [DIM][NV][NPE] (MMA: F_y only)
+  double* sT = sF + OFFT;                                    // [face][HW][L]
+  double* sH = sT + G::FACES * HW * L;                       // [face][NV][L]
+  double* ring = sF + WSL;                                   // [depth][1+NU][NV][NPE] | faces
   const long long nwarps = (long long)gridDim.x * G::WARPS;
   double alpha = 0.0;
   if (lane == 0)
@@ -512,7 +565,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   if constexpr (USE_MMA) {
     ln8.r = r;
     ln8.c = c;
-    ln8.n0 = c + N * r;
+    ln8.n0 = 2 * c + N * r;
     ln8.f = lane >> 3;
     ln8.t = lane & 7;
     // the neighbour's facing node: x-lo (7, t), x-hi (0, t), y-lo (t, 7), y-hi (t, 0)
@@ -523,8 +576,8 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     ln8.yco0 = c == 0 ? p.lift[1] : 0.0;
     ln8.yco1 = c == 3 ? -p.lift[1] : 0.0;
     for (int h = 0; h < 2; ++h) {
-      ln8.kx[h] = p.K[0][r * N + c + 4 * h];
-      ln8.ky[h] = p.K[1][r * N + c + 4 * h];
+      ln8.kx[h] = p.K[0][r * N + 2 * c + h];
+      ln8.ky[h] = p.K[1][r * N + 2 * c + h];
     }
   }
   double kx[2] = {0.0, 0.0}, ky[2] = {0.0, 0.0};

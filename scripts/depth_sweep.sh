@@ -1,5 +1,5 @@
-# ring-depth sweep on the headline workload (tuning)
-for D in auto 0 2 3 4; do
+# ring-depth sweep (tuning): per-stage ms, arith given as $1 (0 exact, 1 fast)
+for D in auto 0 2; do
   if [ $D = auto ]; then unset NDGX_DEPTH; else export NDGX_DEPTH=$D; fi
-  echo "depth=$D $(timeout 120 python scripts/quickbench.py 1 2>&1 | grep 'eq1 o8 rk1 arith1')"
+  timeout 200 python scripts/quickbench.py ${1:-1} 2>&1 | grep 'rk' | cut -c1-210 | sed "s/^/depth=$D /"
 done
