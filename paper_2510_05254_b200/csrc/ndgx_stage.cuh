@@ -478,7 +478,10 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
 template <int DIM, int N, int KIND, bool EXACT, int SIG>
 // <= 128 registers (4 CTAs = 16 warps per SM): capping at 80 for 24 warps
 // measured 25% slower (less load-level parallelism per warp)
-__global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS, 4)
+#ifndef NDGX_MINB
+#define NDGX_MINB 4
+#endif
+__global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS, NDGX_MINB)
 stage_kernel(const __grid_constant__ StageArgs p) {
   using G = Geo<DIM, N, KIND>;
   using A = Ar<EXACT>;

@@ -27,7 +27,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libndgx.so")
+LIB_PATH = os.environ.get("NDGX_LIB") or os.path.join(_PKG, "libndgx.so")  # NDGX_LIB: tuning builds
 
 ADVECTION, EULER_ISOTHERMAL = 0, 1
 RK3, RK4, RK6 = 0, 1, 2
