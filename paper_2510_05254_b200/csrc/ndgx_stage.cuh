@@ -288,6 +288,32 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   const size_t ebase = (size_t)e * CHUNK;
   const double a2 = KIND == 1 ? p.sound_speed : 0.0;
 
+  // face neighbour loads first, so they are in flight together with the
+  // node loads (one memory latency per element instead of two)
+  const int f = ln.f, d = f >> 1, side = f & 1;
+  const bool bnd = d == 0 ? (side ? cx == C0 - 1 : cx == 0) : (side ? cy == C1 - 1 : cy == 0);
+  const double* ext = p.ext[d][side];
+  const bool from_ext = bnd && ext != nullptr;
+  double Nraw[1 + NU][NV];
+  if (!ring) {
+    if (from_ext) {
+      const size_t xs = d == 0 ? (size_t)cy : (size_t)cx;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Nraw[0][v] = __ldg(ext + (xs * NV + v) * L + ln.t);
+    } else {
+      const int step_d = d == 0 ? 1 : C0;
+      const int span = d == 0 ? C0 : C1;
+      const int en = side ? (bnd ? e - (span - 1) * step_d : e + step_d) : (bnd ? e + (span - 1) * step_d : e - step_d);
+      const size_t g = (size_t)en * CHUNK + ln.nb_node;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        Nraw[0][v] = __ldg(p.u + g + v * NPE);
+#pragma unroll
+        for (int a = 0; a < NU; ++a) Nraw[1 + a][v] = __ldg(p.ku[a] + g + v * NPE);
+      }
+    }
+  }
+
   // ---------------------------------------------------------- nodes
   double Bx[2][NV], Fyp[2][NV];
   // both nodes of the lane at once: one 16-byte load per (array, var)
@@ -367,14 +393,10 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
 
   // ---------------------------------------------------------- faces
   {
-    const int f = ln.f, d = f >> 1, side = f & 1;
-    const bool bnd = d == 0 ? (side ? cx == C0 - 1 : cx == 0) : (side ? cy == C1 - 1 : cy == 0);
-    const double* ext = p.ext[d][side];
     double Un[NV];
-    if (bnd && ext != nullptr) {
-      const size_t xs = d == 0 ? (size_t)cy : (size_t)cx;
+    if (from_ext) {
 #pragma unroll
-      for (int v = 0; v < NV; ++v) Un[v] = ring ? fsrc[v * 32 + lane] : __ldg(ext + (xs * NV + v) * L + ln.t);
+      for (int v = 0; v < NV; ++v) Un[v] = ring ? fsrc[v * 32 + lane] : Nraw[0][v];
     } else if (ring) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
@@ -382,14 +404,12 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
         combine_s<false, NU, AM, BM>(p, fsrc + v * 32 + lane, NV * 32, false, Un[v], S);
       }
     } else {
-      const int step_d = d == 0 ? 1 : C0;
-      const int span = d == 0 ? C0 : C1;
-      const int en = side ? (bnd ? e - (span - 1) * step_d : e + step_d) : (bnd ? e + (span - 1) * step_d : e - step_d);
-      const size_t g = (size_t)en * CHUNK + ln.nb_node;
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        double S;
-        combine_g<false, NU, AM, BM>(p, g + v * NPE, false, Un[v], S);
+        Un[v] = Nraw[0][v];
+#pragma unroll
+        for (int a = 0; a < NU; ++a)
+          if ((AM >> a & 1) != 0) Un[v] = fma(p.ca[a], Nraw[1 + a][v], Un[v]);
       }
     }
     double Fn[NV], sn;
