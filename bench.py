@@ -216,11 +216,15 @@ def bench_ours(args):
     cfg = ndgx.SolverConfig(mesh, model, rk, 0.4, 1.0)
     stages = STAGES[rk]
 
-    if world > 1:
+    ranked = world > 1 or args.force_exchange
+    if ranked:
         # NCCL bootstrap over torch.distributed, then one ndgx rank per GPU
+        # (--force-exchange: the same path at world size 1, every axis through NCCL)
         obj = [ndgx.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        s = ndgx.Solver.for_rank(cfg, world, rank, obj[0], device=dev, arith=arith)
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        s = ndgx.Solver.for_rank(cfg, world, rank, obj[0], device=dev, arith=arith,
+                                 force_exchange=args.force_exchange)
         lo, hi = tuple(s.plan.lo), tuple(s.plan.hi)
     else:
         s = ndgx.Solver(cfg, device=dev, arith=arith)
@@ -230,7 +234,7 @@ def bench_ours(args):
     # pinned host state (the reference AoS layout), synthetic IC of this block
     host = torch.empty(dof, dtype=torch.float64, pin_memory=True)
     u0 = host.numpy()
-    if world > 1:
+    if ranked:
         ndgx.init_block(cfg, lo, hi, out=u0)
     elif eq:
         ndgx.init_euler_subsonic(mesh, model, out=u0)
@@ -299,10 +303,12 @@ def bench_ours(args):
     # ---- the bit-identical (reference operation order) mode, same workload ----
     exact = None
     if args.arith == "fast" and not args.no_exact_arm:
-        if world > 1:
+        if ranked:
             obj = [ndgx.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            sx = ndgx.Solver.for_rank(cfg, world, rank, obj[0], device=dev, arith=ndgx.ARITH_EXACT)
+            if world > 1:
+                dist.broadcast_object_list(obj, src=0)
+            sx = ndgx.Solver.for_rank(cfg, world, rank, obj[0], device=dev, arith=ndgx.ARITH_EXACT,
+                                      force_exchange=args.force_exchange)
         else:
             sx = ndgx.Solver(cfg, device=dev, arith=ndgx.ARITH_EXACT)
         sx.upload_ptr(host.data_ptr())
@@ -342,8 +348,10 @@ def bench_ours(args):
                        "arith_note": ("fast = FP64 with FMA contraction and FP64 tensor-core (DMMA) volume "
                                       "quadrature, <= 1e-12 relative L2 vs the reference (tests/test_gpu_parity.py); "
                                       "exact = bit-identical") ,
-                       "parallelism": "1 GPU" if world == 1 else
-                       f"{world} ranks, decompose() blocks {list(s.plan.grid)}, NCCL face-halo exchange per RK stage",
+                       "parallelism": ("1 GPU" if not ranked else
+                                       f"{world} rank(s), decompose() blocks {list(s.plan.grid)}, NCCL face-halo "
+                                       f"exchange per RK stage" + (" (forced on every axis)" if args.force_exchange
+                                                                   else "")),
                        "l2": "no flush needed: each state array (8*dof bytes) exceeds the 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -375,6 +383,8 @@ def main():
     ap.add_argument("--arith", default="fast", choices=["exact", "fast"])
     ap.add_argument("--no-exact-arm", action="store_true", help="skip the bit-exact side measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-exchange", action="store_true",
+                    help="run the multi-GPU rank path even at one rank (every axis through NCCL)")
     args = ap.parse_args()
     if args.impl == "reference":
         bench_reference_arm(args)
