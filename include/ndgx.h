@@ -179,6 +179,14 @@ int ndgx_init_multisine_block(const ndgx_problem* global, const double* amplitud
                               const int hi[3], double* u_aos);
 int ndgx_init_euler_subsonic_block(const ndgx_problem* global, const int lo[3], const int hi[3], double* u_aos);
 
+/* Checkpoint / restart in the reference's field-dump format ("ndgfield 1":
+ * text header, then the raw little-endian doubles in FieldShape::index
+ * order; dump_field / load_field, src/field_io.cpp:18-72).  dump writes the
+ * solver's current state (its block, for a rank solver); load checks the
+ * header against the solver's mesh and uploads the payload. */
+int ndgx_dump_field(ndgx_solver* s, const char* path, ndgx_error* err);
+int ndgx_load_field(ndgx_solver* s, const char* path, ndgx_error* err);
+
 /* Library identification: "ndgx <version> sm_100a". */
 const char* ndgx_version(void);
 

@@ -14,6 +14,7 @@
 
 #include "ndg/basis.hpp"
 #include "ndg/errors.hpp"
+#include "ndg/field_io.hpp"
 #include "ndg/grid.hpp"
 #include "ndg/models.hpp"
 #include "ndg/partition.hpp"
@@ -116,6 +117,15 @@ int ref_init_euler_subsonic(const ndgo_config* c, double* out) {
   ndg::StateField f =
       ndg::init_euler_subsonic(mesh_of(c), model_of(c), ndg::gauss_lobatto(c->order), 0);
   std::memcpy(out, f.data(), f.size() * sizeof(double));
+  return 0;
+}
+
+// dump_field (src/field_io.cpp:18-34) of a host field in FieldShape order
+int ref_dump_field(const ndgo_config* c, const double* u, const char* path) {
+  const ndg::Mesh mesh = mesh_of(c);
+  ndg::StateField f(mesh, model_of(c));
+  std::memcpy(f.data(), u, f.size() * sizeof(double));
+  ndg::dump_field(path, mesh, f);
   return 0;
 }
 

@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <limits>
 #include <new>
 #include <string>
@@ -720,6 +722,86 @@ int ndgx_create_rank(const ndgx_problem* global, int nranks, int rank, const uns
   }
   s->nc = nc;
   return NDGX_OK;
+}
+
+int ndgx_dump_field(ndgx_solver* s, const char* path, ndgx_error* err) {
+  clear_error(err);
+  if (!s || !path) {
+    set_error(err, NDGX_ERR_CONFIG, "null argument");
+    return NDGX_ERR_CONFIG;
+  }
+  std::vector<double> host(s->n);
+  if (int rc = ndgx_download(s, host.data(), err)) return rc;
+  std::ofstream out(path, std::ios::binary);
+  if (!out) {
+    set_error(err, NDGX_ERR_RUN, std::string("cannot open ") + path + " for writing");
+    return NDGX_ERR_RUN;
+  }
+  // the header exactly as dump_field writes it (src/field_io.cpp:18-34)
+  std::ostringstream h;
+  h << "ndgfield 1\n";
+  h << "dim " << s->dim << "\n";
+  h << "cells";
+  for (int a = 0; a < s->dim; ++a) h << " " << s->cells[a];
+  h << "\norder " << s->N << "\n";
+  h << "nvar " << s->nv << "\n";
+  h << "length";
+  for (int a = 0; a < s->dim; ++a) {
+    // a block's extent: its cells times the global cell size
+    const double len = s->cells[a] == s->gcells[a] ? s->p.length[a]
+                                                   : s->cells[a] * (s->p.length[a] / s->gcells[a]);
+    h << " " << len;
+  }
+  h << "\ndata\n";
+  const std::string hs = h.str();
+  out.write(hs.data(), (std::streamsize)hs.size());
+  out.write(reinterpret_cast<const char*>(host.data()), (std::streamsize)(host.size() * sizeof(double)));
+  if (!out) {
+    set_error(err, NDGX_ERR_RUN, std::string("short write to ") + path);
+    return NDGX_ERR_RUN;
+  }
+  return NDGX_OK;
+}
+
+int ndgx_load_field(ndgx_solver* s, const char* path, ndgx_error* err) {
+  clear_error(err);
+  if (!s || !path) {
+    set_error(err, NDGX_ERR_CONFIG, "null argument");
+    return NDGX_ERR_CONFIG;
+  }
+  auto fail = [&](int code, const std::string& m) {
+    set_error(err, code, m);
+    return code;
+  };
+  std::ifstream in(path, std::ios::binary);
+  if (!in) return fail(NDGX_ERR_RUN, std::string("cannot open ") + path);
+  std::string line;
+  if (!std::getline(in, line) || line != "ndgfield 1")
+    return fail(NDGX_ERR_RUN, std::string(path) + ": not an ndgfield dump");
+  int dim = 0, order = 0, nvar = 0, cells[3] = {1, 1, 1};
+  while (std::getline(in, line)) {  // load_field (src/field_io.cpp:36-72)
+    if (line == "data") break;
+    std::istringstream ls(line);
+    std::string key;
+    ls >> key;
+    double len;
+    if (key == "dim") ls >> dim;
+    else if (key == "cells") for (int a = 0; a < dim && a < 3; ++a) ls >> cells[a];
+    else if (key == "order") ls >> order;
+    else if (key == "nvar") ls >> nvar;
+    else if (key == "length") for (int a = 0; a < dim && a < 3; ++a) ls >> len;
+    else return fail(NDGX_ERR_RUN, std::string(path) + ": unknown header key '" + key + "'");
+    if (!ls) return fail(NDGX_ERR_RUN, std::string(path) + ": malformed header line '" + line + "'");
+  }
+  if (line != "data") return fail(NDGX_ERR_RUN, std::string(path) + ": missing data section");
+  bool same = dim == s->dim && order == s->N && nvar == s->nv;
+  for (int a = 0; a < s->dim; ++a) same = same && cells[a] == s->cells[a];
+  if (!same) return fail(NDGX_ERR_CONFIG, std::string(path) + ": field shape does not match the solver's mesh");
+  std::vector<double> host(s->n);
+  in.read(reinterpret_cast<char*>(host.data()), (std::streamsize)(host.size() * sizeof(double)));
+  if (in.gcount() != (std::streamsize)(host.size() * sizeof(double)))
+    return fail(NDGX_ERR_RUN, std::string(path) + ": truncated payload");
+  return ndgx_upload(s, host.data(), err);
 }
 
 int ndgx_get_plan(const ndgx_solver* s, ndgx_rank_plan* plan) {

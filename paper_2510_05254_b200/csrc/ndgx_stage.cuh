@@ -483,8 +483,10 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
           record_error(p.ctl, error_key(step + 1, kPhaseScan, (gx * p.gcells[1] + gy) * (long long)p.gcells[2],
                                         (n & 7) * N + (n >> 3)));
         } else {
+          // the same IEEE expression as alpha_scan_kernel, so a restarted run
+          // (whose first alpha comes from the scan) reproduces dt bit for bit
           const double mm = dmax(fabs(un[s2][1]), fabs(un[s2][2]));
-          alpha = dmax(alpha, fma(mm, fast_rcp(un[s2][0]), p.sound_speed));
+          alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[s2][0]), p.sound_speed));
         }
       }
     }
@@ -831,7 +833,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
               double mm = 0.0;
 #pragma unroll
               for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[s2][1 + d]));
-              alpha = dmax(alpha, fma(mm, fast_rcp(un[s2][0]), p.sound_speed));  // contracted mode
+              alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[s2][0]), p.sound_speed));  // == alpha_scan_kernel
             }
           }
         }

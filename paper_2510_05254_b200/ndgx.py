@@ -148,6 +148,8 @@ def lib() -> C.CDLL:
     L.ndgx_nccl_unique_id.argtypes = [C.c_char_p, P(Error)]
     L.ndgx_create_rank.argtypes = [P(Problem), C.c_int, C.c_int, C.c_char_p, C.c_int, P(C.c_void_p), P(Error)]
     L.ndgx_get_plan.argtypes = [C.c_void_p, P(RankPlan)]
+    L.ndgx_dump_field.argtypes = [C.c_void_p, C.c_char_p, P(Error)]
+    L.ndgx_load_field.argtypes = [C.c_void_p, C.c_char_p, P(Error)]
     L.ndgx_init_multisine_block.argtypes = [P(Problem), D, C.c_int, P(C.c_int), P(C.c_int), D]
     L.ndgx_init_euler_subsonic_block.argtypes = [P(Problem), P(C.c_int), P(C.c_int), D]
     _lib = L
@@ -424,6 +426,17 @@ class Solver:
         _check(lib().ndgx_profile_step(self._h, ms, 16, C.byref(err)), err)
         return [ms[i] for i in range(self.stages)], ms[self.stages]
 
+    def dump_field(self, path: str) -> None:
+        """Checkpoint the device state in the reference's ndgfield format
+        (dump_field, src/field_io.cpp:18-34)."""
+        err = Error()
+        _check(lib().ndgx_dump_field(self._h, os.fsencode(path), C.byref(err)), err)
+
+    def load_field(self, path: str) -> None:
+        """Restart from an ndgfield dump (load_field, src/field_io.cpp:36-72)."""
+        err = Error()
+        _check(lib().ndgx_load_field(self._h, os.fsencode(path), C.byref(err)), err)
+
     @property
     def stream(self) -> int:
         return int(lib().ndgx_stream(self._h) or 0)
@@ -585,6 +598,50 @@ def init_block(config: SolverConfig, lo, hi, n_modes: int = 40, seed: int = 42,
     if rc != 0:
         raise ConfigError("init_block: invalid block or model")
     return out
+
+
+def dump_field(path: str, mesh: Mesh, field) -> None:
+    """dump_field(path, mesh, field) (src/field_io.cpp:18-34) for a host field."""
+    f = np.ascontiguousarray(field, dtype="<f8")
+    lines = ["ndgfield 1", f"dim {mesh.dim}", "cells " + " ".join(str(mesh.cells[a]) for a in range(mesh.dim)),
+             f"order {mesh.order}", f"nvar {f.size // (mesh.cell_count() * mesh.nodes_per_cell())}",
+             "length " + " ".join(_fmt_g6(mesh.length[a]) for a in range(mesh.dim)), "data"]
+    with open(path, "wb") as fh:
+        fh.write(("\n".join(lines) + "\n").encode())
+        fh.write(f.tobytes())
+
+
+def load_field(path: str):
+    """load_field(path) (src/field_io.cpp:36-72) -> (dim, cells, order, nvar, length, field)."""
+    with open(path, "rb") as fh:
+        if fh.readline() != b"ndgfield 1\n":
+            raise RuntimeError(f"{path}: not an ndgfield dump")
+        hdr = {}
+        while True:
+            line = fh.readline()
+            if not line:
+                raise RuntimeError(f"{path}: missing data section")
+            line = line.decode().rstrip("\n")
+            if line == "data":
+                break
+            key, *vals = line.split()
+            if key not in ("dim", "cells", "order", "nvar", "length"):
+                raise RuntimeError(f"{path}: unknown header key '{key}'")
+            hdr[key] = vals
+        payload = fh.read()
+    dim = int(hdr["dim"][0])
+    cells = tuple(int(x) for x in hdr["cells"][:dim])
+    order, nvar = int(hdr["order"][0]), int(hdr["nvar"][0])
+    n = nvar * order ** dim * int(np.prod(cells))
+    if len(payload) < 8 * n:
+        raise RuntimeError(f"{path}: truncated payload")
+    return dim, cells, order, nvar, tuple(float(x) for x in hdr["length"][:dim]), \
+        np.frombuffer(payload[:8 * n], dtype="<f8").copy()
+
+
+def _fmt_g6(x: float) -> str:
+    """std::ostream's default double formatting (precision 6, %g)."""
+    return f"{x:g}"
 
 
 def version() -> str:
