@@ -13,11 +13,11 @@ struct StageKernel {
   StageFn fn[kNumSigs] = {};  // by stage signature (kSigs)
   int threads = 0;
   int warps = 0;            // elements in flight per CTA (one per warp)
-  int smem_fixed = 0;       // dynamic shared memory without the element rings
+  int smem_fixed[kNumSigs] = {};  // dynamic shared memory without the element rings, per signature
   int ring_per_array = 0;   // ring bytes per slot per input array (all warps of a CTA)
   bool tma_ok = false;      // element chunks are 16-byte multiples (bulk copies)
   bool prefer_direct = false;  // measured: direct loads beat the TMA ring (Euler, B200)
-  int smem(int nu, int depth) const { return smem_fixed + depth * (1 + nu) * ring_per_array; }
+  int smem(int sig, int depth) const { return smem_fixed[sig] + depth * (1 + kSigs[sig].nu) * ring_per_array; }
 };
 
 // Launch configuration of one stage kernel variant (host side).
@@ -43,13 +43,14 @@ StageKernel make_stage_kernel() {
   k.fn[8] = &stage_kernel<DIM, N, KIND, EXACT, 8>;
   k.threads = G::THREADS;
   k.warps = G::WARPS;
-  k.smem_fixed = G::smem_bytes(0, 0, G::MMA && !EXACT);
+  for (int q = 0; q < kNumSigs; ++q)
+    k.smem_fixed[q] = G::smem_bytes(0, 0, G::mma_body(EXACT, kSigs[q].nu), kSigs[q].bm != 0);
   k.ring_per_array = G::WARPS * G::SLOT1 * 8;
   k.tma_ok = G::TMA_OK;
   // Euler stages: 16 warps/SM of 16-byte direct loads keep more bytes in flight
   // than a per-warp TMA ring, whose shared memory costs resident warps
   // (C3 fast 3.22 vs 4.21 ms/step, exact 6.70 vs 6.8; profiles/README.md)
-  k.prefer_direct = KIND == 1;
+  k.prefer_direct = KIND == 1 || G::MMA3;
   return k;
 }
 

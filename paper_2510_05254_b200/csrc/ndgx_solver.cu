@@ -340,7 +340,7 @@ struct ndgx_solver {
       for (int d = (kern.tma_ok && (!kern.prefer_direct || forced > 0)) ? 4 : 0; d >= 0; --d) {
         if (d == 1) continue;  // a ring needs one slot ahead
         if (forced >= 0 && d != forced && !(d == 0 && !kern.tma_ok)) continue;
-        const int bytes = kern.smem(nu, d);
+        const int bytes = kern.smem(q, d);
         if (bytes > limit) continue;
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attribute");
         int per_sm = 0;

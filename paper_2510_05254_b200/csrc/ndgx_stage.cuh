@@ -65,17 +65,28 @@ struct Geo {
   static constexpr int HEAD = WARPS * MAXD + RED;            // 8-byte words before the slabs
   static constexpr int CHUNK = NV * NPE;                     // one array of one element (doubles)
   static constexpr bool TMA_OK = (CHUNK % 2) == 0;           // 16-byte element chunks
-  static constexpr bool MMA = (DIM == 2 && N == 8);          // FAST-mode tensor-core volume
+  static constexpr bool MMA = (DIM == 2 && N == 8);          // FAST-mode tensor-core volume (2D)
+  static constexpr bool MMA3 = (DIM == 3 && N == 4);         // FAST-mode tensor-core volume (3D)
   // one face node per lane: the ring slot also carries the element's face
   // neighbour values ([array][var][lane], cp.async), so no load is on demand
   static constexpr bool FACE_PF = (FM == 1);
   static constexpr int SLOT1 = CHUNK + (FACE_PF ? 32 * NV : 0);  // ring doubles per input array
-  // the tensor-core body stages only F_y (F_x stays in registers as MMA fragments)
-  static constexpr __host__ __device__ int wslab(bool mma) {
-    return mma ? (((2 * NV * NPE + FACES * HW * L + FACES * NV * L) + 1) & ~1) : WSLAB;
+  // tensor-core bodies: 2D stages only F_y (F_x stays in registers as MMA
+  // fragments); 3D stages F_x, F_y, F_z (F_x becomes the accumulator) and
+  // keeps face traces of U and speed only.  Both add S at the last stage.
+  static constexpr __host__ __device__ int wslab(bool mma, bool last) {
+    return mma ? (MMA3 ? (((3 + (last ? 1 : 0)) * NV * NPE + FACES * (NV + 1) * L + FACES * NV * L + 1) & ~1)
+                       : (((1 + (last ? 1 : 0)) * NV * NPE + FACES * HW * L + FACES * NV * L + 1) & ~1))
+               : WSLAB;
   }
-  static constexpr int smem_bytes(int nu, int depth, bool mma) {
-    return (HEAD + WARPS * (wslab(mma) + depth * (1 + nu) * SLOT1)) * 8;
+  // which body a (arith, signature) kernel runs: the 2D N=8 / 3D N=4
+  // tensor-core bodies (contracted mode; 3D only for stages reading <= 1
+  // K_j -- the RK6 stages with more terms keep the generic body, measured)
+  static constexpr __host__ __device__ bool mma_body(bool exact, int nu) {
+    return !exact && (MMA || (MMA3 && nu <= 1));
+  }
+  static constexpr int smem_bytes(int nu, int depth, bool mma, bool last) {
+    return (HEAD + WARPS * (wslab(mma, last) + depth * (1 + nu) * SLOT1)) * 8;
   }
 
   // node index of position k along `axis` on transverse line t
@@ -256,6 +267,250 @@ __device__ __forceinline__ void combine_pair(const StageArgs& p, bool ring, cons
     *S0 = a;
     *S1 = b;
   }
+}
+
+// ------------------------------------------------------------ 3D order-4 body
+// One element of the 3D, N = 4, contracted-arithmetic stage (the C4 shape).
+// Per axis d the volume term is D_d[k][line] = sum_l K_d[k][l] F_d[l][line]
+// over the 16 lines of the axis, two m8n8k4 MMAs (lines 0-7, 8-15; rows
+// 4-7 of A are zero), with the running sum over axes carried through the
+// MMA accumulator input from shared memory (F_x's slots hold it).
+struct Lane4 {
+  double k[3];  // K_d[r][c] (0 for r >= 4)
+};
+
+template <int KIND, int NU, int AM, int BM>
+__device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4& ln, int lane, int e, int cx,
+                                                 int cy, int cz, double* sF, double* sT, double* sH, double dt,
+                                                 long long step, double& alpha) {
+  constexpr int N = 4, NPE = 64, L = 16, DIM = 3;
+  constexpr int NV = KIND == 0 ? 1 : 4;
+  constexpr int TW = NV + 1;  // trace record: U, one-sided speed
+  constexpr int CHUNK = NV * NPE;
+  constexpr bool LAST = BM != 0;
+  using G = Geo<3, 4, KIND>;
+  const int C0 = p.cells[0], C1 = p.cells[1], C2 = p.cells[2];
+  const size_t ebase = (size_t)e * CHUNK;
+  const double a2 = KIND == 1 ? p.sound_speed : 0.0;
+  const int r = lane >> 2, c = lane & 3;
+  double* sS = sF + 3 * NV * NPE;  // last stage: S at the nodes
+
+  // flux of U along axis d and the one-sided speed (models.cpp:42-70), contracted
+  auto fluxd = [&](const double* U, int d, double* F, double& sp) {
+    if (KIND == 0) {
+      F[0] = p.vel[d] * U[0];
+      sp = fabs(p.vel[d]);
+    } else {
+      const double rinv = fast_rcp(U[0]);
+      const double ua = U[1 + d] * rinv;
+      const double pr = U[0] * a2 * a2;
+      F[0] = U[1 + d];
+#pragma unroll
+      for (int q = 1; q < NV; ++q) F[q] = ua * U[q];
+      F[1 + d] += pr;
+      sp = fabs(ua) + a2;
+    }
+  };
+
+  // ---------------------------------------------------------- nodes (pair 2 lane, 2 lane + 1)
+  {
+    const int n0 = 2 * lane;
+    double Up[2][NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const size_t g = ebase + v * NPE + n0;
+      double2 k[1 + NU];
+      k[0] = __ldg(reinterpret_cast<const double2*>(p.u + g));
+#pragma unroll
+      for (int t = 0; t < NU; ++t) k[1 + t] = __ldg(reinterpret_cast<const double2*>(p.ku[t] + g));
+      double u0 = k[0].x, u1 = k[0].y;
+#pragma unroll
+      for (int t = 0; t < NU; ++t)
+        if ((AM >> t & 1) != 0) {
+          u0 = fma(p.ca[t], k[1 + t].x, u0);
+          u1 = fma(p.ca[t], k[1 + t].y, u1);
+        }
+      Up[0][v] = u0;
+      Up[1][v] = u1;
+      if (LAST) {
+        double s0 = k[0].x, s1 = k[0].y;
+#pragma unroll
+        for (int t = 0; t < NU; ++t)
+          if ((BM >> t & 1) != 0) {
+            s0 = fma(p.cb[t], k[1 + t].x, s0);
+            s1 = fma(p.cb[t], k[1 + t].y, s1);
+          }
+        *reinterpret_cast<double2*>(sS + v * NPE + n0) = make_double2(s0, s1);
+      }
+    }
+    double Fp[DIM][2][NV];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int n = n0 + h;
+      if (KIND == 1 && !(Up[h][0] > 0.0)) {
+        const int i = n & 3, j = (n >> 2) & 3, kk = n >> 4;
+        const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
+        record_error(p.ctl, error_key(step, p.phase, (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz,
+                                      (j * N + kk) * N + i));
+      }
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double sp;
+        fluxd(Up[h], d, Fp[d][h], sp);
+        const int pos = G::pos_of(d, n);
+        if (pos == 0 || pos == N - 1) {
+          double* t = sT + ((2 * d + (pos == 0 ? 0 : 1)) * TW) * L + G::line_of(d, n);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) t[v * L] = Up[h][v];
+          t[NV * L] = sp;
+        }
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        *reinterpret_cast<double2*>(sF + (d * NV + v) * NPE + n0) = make_double2(Fp[d][0][v], Fp[d][1][v]);
+  }
+  __syncwarp();
+
+  // ---------------------------------------------------------- faces (96 nodes, 3 per lane)
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    const int q = lane + 32 * m;
+    const int f = q >> 4, t = q & 15;
+    const int d = f >> 1, side = f & 1;
+    const int ca = d == 0 ? cx : (d == 1 ? cy : cz);
+    const int cn = d == 0 ? C0 : (d == 1 ? C1 : C2);
+    const bool bnd = side ? (ca == cn - 1) : (ca == 0);
+    const double* ext = p.ext[d][side];
+    double Un[NV];
+    if (bnd && ext != nullptr) {
+      const size_t xs = d == 0 ? (size_t)cy + (size_t)C1 * cz
+                               : (d == 1 ? (size_t)cx + (size_t)C0 * cz : (size_t)cx + (size_t)C0 * cy);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Un[v] = __ldg(ext + (xs * NV + v) * L + t);
+    } else {
+      const int stride = d == 0 ? 1 : (d == 1 ? C0 : C0 * C1);
+      const int en = side ? (bnd ? e - (cn - 1) * stride : e + stride) : (bnd ? e + (cn - 1) * stride : e - stride);
+      const size_t g = (size_t)en * CHUNK + G::node(d, t, side ? 0 : N - 1);
+      // all of this node's loads in flight first, then the combination
+      double raw[1 + NU][NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        raw[0][v] = __ldg(p.u + g + v * NPE);
+#pragma unroll
+        for (int a = 0; a < NU; ++a)
+          if ((AM >> a & 1) != 0) raw[1 + a][v] = __ldg(p.ku[a] + g + v * NPE);
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        Un[v] = raw[0][v];
+#pragma unroll
+        for (int a = 0; a < NU; ++a)
+          if ((AM >> a & 1) != 0) Un[v] = fma(p.ca[a], raw[1 + a][v], Un[v]);
+      }
+    }
+    double Uo[NV];
+    const double* tr = sT + (f * TW) * L + t;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) Uo[v] = tr[v * L];
+    const double so = tr[NV * L];
+    double Fo[NV], Fn[NV], sn, dummy;
+    fluxd(Uo, d, Fo, dummy);
+    fluxd(Un, d, Fn, sn);
+    const double al = dmax(so, sn);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
+      const double um = side ? Uo[v] : Un[v], up = side ? Un[v] : Uo[v];
+      const double fm = side ? Fo[v] : Fn[v], fp = side ? Fn[v] : Fo[v];
+      sH[(f * NV + v) * L + t] = 0.5 * ((fm + fp) - al * (up - um));
+    }
+  }
+  __syncwarp();
+
+  // ---------------------------------------------------------- volume on the tensor cores
+  double* acc = sF;  // F_x's slots become the running dudt
+  const bool krow = r < N;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    if (d > 0) __syncwarp();  // the previous axis' partial sums are stored
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const int o0 = G::node(d, 8 * g + 2 * c, r), o1 = G::node(d, 8 * g + 2 * c + 1, r);
+        double c0 = 0.0, c1 = 0.0;
+        if (d > 0 && krow) {
+          c0 = acc[v * NPE + o0];
+          c1 = acc[v * NPE + o1];
+        }
+        const double b = sF[(d * NV + v) * NPE + G::node(d, 8 * g + r, c)];
+        dmma_8x8x4(ln.k[d], b, c0, c1);
+        if (d < DIM - 1) {
+          __syncwarp();  // B/C reads of this group precede the in-place stores
+          if (krow) {
+            acc[v * NPE + o0] = c0;
+            acc[v * NPE + o1] = c1;
+          }
+        } else if (krow) {
+          // final axis: outputs at nodes o0, o0 + 1 = line + 16 r; lifted faces
+          double dv[2] = {c0, c1};
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2) {
+            const int n = s2 ? o1 : o0;
+            const int i = n & 3, j = (n >> 2) & 3, kk = n >> 4;
+            if (i == 0) dv[s2] = fma(p.lift[0], sH[(0 * NV + v) * L + j + 4 * kk], dv[s2]);
+            if (i == N - 1) dv[s2] = fma(-p.lift[0], sH[(1 * NV + v) * L + j + 4 * kk], dv[s2]);
+            if (j == 0) dv[s2] = fma(p.lift[1], sH[(2 * NV + v) * L + i + 4 * kk], dv[s2]);
+            if (j == N - 1) dv[s2] = fma(-p.lift[1], sH[(3 * NV + v) * L + i + 4 * kk], dv[s2]);
+            if (kk == 0) dv[s2] = fma(p.lift[2], sH[(4 * NV + v) * L + i + 4 * j], dv[s2]);
+            if (kk == N - 1) dv[s2] = fma(-p.lift[2], sH[(5 * NV + v) * L + i + 4 * j], dv[s2]);
+          }
+          const double k0 = dv[0] * dt, k1 = dv[1] * dt;
+          double* gout = p.out + ebase + v * NPE + o0;  // o1 == o0 + 1
+          if (!LAST) {
+            *reinterpret_cast<double2*>(gout) = make_double2(k0, k1);
+          } else {
+            const double u0 = fma(p.b_last, k0, sS[v * NPE + o0]);
+            const double u1 = fma(p.b_last, k1, sS[v * NPE + o1]);
+            *reinterpret_cast<double2*>(gout) = make_double2(u0, u1);
+            acc[v * NPE + o0] = u0;  // u_new for the finite check / next alpha
+            acc[v * NPE + o1] = u1;
+          }
+        }
+      }
+    }
+  }
+  if (LAST) {
+    __syncwarp();
+    // node-parallel over the lane's own pair: finite check and next alpha
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int n = 2 * lane + h;
+      double un[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) un[v] = acc[v * NPE + n];
+      double sum = un[0];
+#pragma unroll
+      for (int v = 1; v < NV; ++v) sum += un[v];
+      if (!isfinite(sum)) record_error(p.ctl, error_key(step, kPhaseInstability, 0, 0));
+      if (KIND == 1 && p.scan_alpha) {
+        if (!(un[0] > 0.0)) {
+          const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
+          record_error(p.ctl, error_key(step + 1, kPhaseScan, (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz,
+                                        G::aos_node(n)));
+        } else {
+          double mm = 0.0;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[1 + d]));
+          alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[0]), p.sound_speed));  // == alpha_scan_kernel
+        }
+      }
+    }
+  }
+  __syncwarp();  // this element's slab reads precede the next element's writes
 }
 
 // ------------------------------------------------------------ flagship body
@@ -509,6 +764,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   using A = Ar<EXACT>;
   constexpr int NV = G::NV, L = G::L, NPE = G::NPE, HW = G::HW;
   constexpr bool USE_MMA = G::MMA && !EXACT;
+  constexpr bool USE_MMA3 = G::MMA3 && G::mma_body(EXACT, kSigs[SIG].nu);
   constexpr int NU = kSigs[SIG].nu, AM = kSigs[SIG].am, BM = kSigs[SIG].bm;
   extern __shared__ __align__(16) double smem[];
 
@@ -529,11 +785,15 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   constexpr int SLOT = (1 + NU) * G::SLOT1;  // one ring slot (doubles): arrays | face neighbour values
   const int depth = G::TMA_OK ? p.depth : 0;  // 0: the node phase reads HBM directly
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + wib * G::MAXD;
-  constexpr int WSL = G::wslab(USE_MMA);
-  constexpr int OFFT = USE_MMA ? 2 * NV * NPE : G::OFF_T;  // MMA: F_y | S
-  double* sF = smem + G::HEAD + wib * (WSL + depth * SLOT);  // [DIM][NV][NPE] (MMA: F_y only)
-  double* sT = sF + OFFT;                                    // [face][HW][L]
-  double* sH = sT + G::FACES * HW * L;                       // [face][NV][L]
+  constexpr bool LASTC = kSigs[SIG].bm != 0;
+  constexpr int WSL = G::wslab(USE_MMA || USE_MMA3, LASTC);
+  // slab: fluxes (2D MMA: F_y; 3D MMA: F_x|F_y|F_z) | S (last stage) | traces | face fluxes
+  constexpr int OFFT = USE_MMA ? (1 + (LASTC ? 1 : 0)) * NV * NPE
+                               : (USE_MMA3 ? (3 + (LASTC ? 1 : 0)) * NV * NPE : G::OFF_T);
+  constexpr int TRW = USE_MMA3 ? NV + 1 : HW;                // trace record width
+  double* sF = smem + G::HEAD + wib * (WSL + depth * SLOT);
+  double* sT = sF + OFFT;                                    // [face][TRW][L]
+  double* sH = sT + G::FACES * TRW * L;                      // [face][NV][L]
   double* ring = sF + WSL;                                   // [depth][1+NU][NV][NPE] | faces
   const long long nwarps = (long long)gridDim.x * G::WARPS;
   double alpha = 0.0;
@@ -586,6 +846,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 
   // MMA lane roles (2D N=8): lane = 4r + c
   const int r = lane >> 2, c = lane & 3;
+  Lane4 ln4{};
+  if constexpr (USE_MMA3) {
+    for (int d = 0; d < 3; ++d) ln4.k[d] = r < 4 ? p.K[d][r * 4 + c] : 0.0;
+  }
   Lane8 ln8{};
   if constexpr (USE_MMA) {
     ln8.r = r;
@@ -660,6 +924,11 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         else if (depth == 3) cp_async_wait<2>();
         else cp_async_wait<3>();
       }
+    }
+    if constexpr (USE_MMA3) {
+      element_3d4_fast<KIND, NU, AM, BM>(p, ln4, lane, e, cx, cy, cz, sF, sT, sH, dt, step, alpha);
+      step_coords(cx, cy, cz);
+      continue;
     }
     if constexpr (USE_MMA) {
       element_2d8_fast<KIND, NU, AM, BM>(p, ln8, lane, e, cx, cy, src, fsrc, depth > 0, sF, sT, sH, dt, last, step,
