@@ -210,7 +210,8 @@ def bench_ours(args):
     # weak scaling: every GPU owns the configuration's mesh; N GPUs stack N
     # copies along the last axis (decompose() then gives slabs, one per rank)
     gcells = list(cells)
-    gcells[dim - 1] *= world
+    if not args.strong:
+        gcells[dim - 1] *= world
     mesh = ndgx.Mesh(dim, tuple(gcells), order)
     model = ndgx.EquationModel.isothermal_euler(dim, 1.0) if eq else ndgx.EquationModel.advection(dim, (1, 0, 0))
     cfg = ndgx.SolverConfig(mesh, model, rk, 0.4, 1.0)
@@ -230,6 +231,7 @@ def bench_ours(args):
         s = ndgx.Solver(cfg, device=dev, arith=arith)
         lo, hi = (0, 0, 0), tuple(mesh.cells)
     dof = s.dof  # this rank's block
+    dof_total = mesh.dof(model)  # all ranks (weak: world * dof; strong: the configuration's mesh)
 
     # pinned host state (the reference AoS layout), synthetic IC of this block
     host = torch.empty(dof, dtype=torch.float64, pin_memory=True)
@@ -263,7 +265,7 @@ def bench_ours(args):
         t = torch.tensor([t_dev], dtype=torch.float64, device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_dev = float(t.item())
-    value = world * dof * stages * args.steps / t_dev
+    value = dof_total * stages * args.steps / t_dev
 
     # ---- kernel-level timing for the roofline (events around each stage) ----
     stage_ms = []
@@ -297,7 +299,7 @@ def bench_ours(args):
         t = torch.tensor([t_e2e], dtype=torch.float64, device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_e2e = float(t.item())
-    e2e = world * dof * stages * st_e.steps / t_e2e
+    e2e = dof_total * stages * st_e.steps / t_e2e
     s.close()
 
     # ---- the bit-identical (reference operation order) mode, same workload ----
@@ -324,7 +326,7 @@ def bench_ours(args):
             t = torch.tensor([tx], dtype=torch.float64, device=f"cuda:{dev}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tx = float(t.item())
-        exact = {"value": world * dof * stages * args.steps / tx, "unit": UNIT,
+        exact = {"value": dof_total * stages * args.steps / tx, "unit": UNIT,
                  "ms_per_step": tx / args.steps * 1e3,
                  "note": "arith=exact: the reference's IEEE operation order, states bit-identical to the CPU reference"}
         sx.close()
@@ -341,10 +343,10 @@ def bench_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (init_euler_subsonic IC of the reference, generated on the host)",
             "config": {"workload": desc, "cells": list(cells), "global_cells": gcells, "order": order,
-                       "rk": RK_NAME[rk], "dof": dof, "dof_total": dof * world, "arith": args.arith,
+                       "rk": RK_NAME[rk], "dof": dof, "dof_total": dof_total, "arith": args.arith,
                        "arith_note": ("fast = FP64 with FMA contraction and FP64 tensor-core (DMMA) volume "
                                       "quadrature, <= 1e-12 relative L2 vs the reference (tests/test_gpu_parity.py); "
                                       "exact = bit-identical") ,
@@ -383,6 +385,9 @@ def main():
     ap.add_argument("--arith", default="fast", choices=["exact", "fast"])
     ap.add_argument("--no-exact-arm", action="store_true", help="skip the bit-exact side measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the configuration's mesh is split across the N GPUs (C5) "
+                         "instead of stacking N copies (weak scaling, the default)")
     ap.add_argument("--force-exchange", action="store_true",
                     help="run the multi-GPU rank path even at one rank (every axis through NCCL)")
     args = ap.parse_args()
