@@ -153,11 +153,19 @@ __device__ __forceinline__ void flux(const StageArgs& p, const double* u, int ax
   } else {
     constexpr int NV = DIM + 1;
     const double rho = u[0];
-    const double ua = (!EXACT && rinv >= 0.0) ? u[1 + axis] * rinv : A::div(u[1 + axis], rho);
-    f[0] = u[1 + axis];
+    // m_axis by selects: `axis` may be a run-time value, and a dynamic index
+    // into u[] / f[] would put both arrays in local memory
+    double ma = u[1];
+    if (axis == 1) ma = u[2];
+    if (DIM > 2 && axis == 2) ma = u[DIM > 2 ? 3 : 1];
+    const double ua = (!EXACT && rinv >= 0.0) ? ma * rinv : A::div(ma, rho);
+    const double pr = A::mul(A::mul(rho, p.sound_speed), p.sound_speed);
+    f[0] = ma;
 #pragma unroll
-    for (int i = 1; i < NV; ++i) f[i] = A::mul(ua, u[i]);
-    f[1 + axis] = A::add(f[1 + axis], A::mul(A::mul(rho, p.sound_speed), p.sound_speed));
+    for (int i = 1; i < NV; ++i) {
+      f[i] = A::mul(ua, u[i]);
+      if (i == 1 + axis) f[i] = A::add(f[i], pr);
+    }
     speed = A::add(fabs(ua), p.sound_speed);
   }
 }

@@ -302,12 +302,12 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
       sp = fabs(p.vel[d]);
     } else {
       const double rinv = fast_rcp(U[0]);
-      const double ua = U[1 + d] * rinv;
+      const double md = d == 0 ? U[1] : (d == 1 ? U[2] : U[NV - 1]);  // selects, not a dynamic index
+      const double ua = md * rinv;
       const double pr = U[0] * a2 * a2;
-      F[0] = U[1 + d];
+      F[0] = md;
 #pragma unroll
-      for (int q = 1; q < NV; ++q) F[q] = ua * U[q];
-      F[1 + d] += pr;
+      for (int q = 1; q < NV; ++q) F[q] = q == 1 + d ? fma(ua, U[q], pr) : ua * U[q];
       sp = fabs(ua) + a2;
     }
   };
@@ -673,9 +673,10 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       sn = fabs(p.vel[d]);
     } else {
       const double rinv = fast_rcp(Un[0]);
-      const double ua = Un[1 + d] * rinv;
+      const double md = d == 0 ? Un[1] : Un[2];  // a select, not a (local-memory) dynamic index
+      const double ua = md * rinv;
       const double pr = Un[0] * a2 * a2;
-      Fn[0] = Un[1 + d];
+      Fn[0] = md;
       Fn[1] = d == 0 ? fma(ua, Un[1], pr) : ua * Un[1];
       Fn[2] = d == 0 ? ua * Un[2] : fma(ua, Un[2], pr);
       sn = fabs(ua) + a2;
