@@ -910,14 +910,6 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       ln8.ky[h] = p.K[1][r * N + 2 * c + h];
     }
   }
-  double kx[2] = {0.0, 0.0}, ky[2] = {0.0, 0.0};
-  if constexpr (USE_MMA) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      kx[h] = p.K[0][r * N + c + 4 * h];  // A of D_x = K_x F_x: K_x[k=r][i=c+4h]
-      ky[h] = p.K[1][r * N + c + 4 * h];  // B of D_y = F_y K_y^T: K_y[k=r][j=c+4h]
-    }
-  }
 
   // element e = cx + C0 (cy + C1 cz), advanced by the total warp count with
   // an incremental (x, y, z) counter (element counts are < 2^31)
@@ -1005,21 +997,20 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     };
 
     // ------------------------------------------------ 1: nodes
-    // lane's nodes: n = lane + 32m (generic) or n = (c + 4h) + 8r (MMA)
-    double Bx[G::NM][NV];  // MMA: F_x at the lane's nodes = B fragments of D_x
-    double Sn[G::NM][NV];  // last stage: S at the lane's output nodes (generic)
+    // lane's nodes: n = lane + 32m
+    double Sn[G::NM][NV];  // last stage: S at the lane's nodes
 #pragma unroll
     for (int m = 0; m < G::NM; ++m) {
-      const int n = USE_MMA ? (c + 4 * m) + N * r : lane + 32 * m;
+      const int n = lane + 32 * m;
       if (n >= NPE) continue;
       double U[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         double S;
         if (depth > 0)
-          combine_s<EXACT, NU, AM, BM>(p, src + v * NPE + n, G::CHUNK, last && !USE_MMA, U[v], S);
+          combine_s<EXACT, NU, AM, BM>(p, src + v * NPE + n, G::CHUNK, last, U[v], S);
         else
-          combine_g<EXACT, NU, AM, BM>(p, ebase + (size_t)v * NPE + n, last && !USE_MMA, U[v], S);
+          combine_g<EXACT, NU, AM, BM>(p, ebase + (size_t)v * NPE + n, last, U[v], S);
         Sn[m][v] = S;
       }
       if (KIND == 1 && !(U[0] > 0.0)) {
@@ -1033,13 +1024,8 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       for (int d = 0; d < DIM; ++d) {
         double F[NV], sp;
         flux<DIM, KIND, EXACT>(p, U, d, F, sp, rinv);
-        if (USE_MMA && d == 0) {
 #pragma unroll
-          for (int v = 0; v < NV; ++v) Bx[m][v] = F[v];
-        } else {
-#pragma unroll
-          for (int v = 0; v < NV; ++v) sF[(d * NV + v) * NPE + n] = F[v];
-        }
+        for (int v = 0; v < NV; ++v) sF[(d * NV + v) * NPE + n] = F[v];
         const int k = G::pos_of(d, n);
         if (k == 0 || k == N - 1) {
           double* t = sT + ((2 * d + (k == 0 ? 0 : 1)) * HW) * L + G::line_of(d, n);
@@ -1107,111 +1093,50 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     __syncwarp();
 
     // ------------------------------------------------ 3: volume, faces, epilogue
-    if constexpr (USE_MMA) {
-      // outputs at nodes (i = r, j = 2c + s), all variables
-      const double xco = r == 0 ? p.lift[0] : (r == N - 1 ? -p.lift[0] : 0.0);
-      const int xf = r == N - 1 ? 1 : 0;
-      const double yco[2] = {c == 0 ? p.lift[1] : 0.0, c == 3 ? -p.lift[1] : 0.0};
-      const int yf[2] = {2, 3};
-      double un[2][NV];
+#pragma unroll
+    for (int m = 0; m < G::NM; ++m) {
+      const int n = lane + 32 * m;
+      if (n >= NPE) continue;
+      double un[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        double d0 = 0.0, d1 = 0.0;
-        dmma_8x8x4(kx[0], Bx[0][v], d0, d1);  // D_x = K_x F_x
-        dmma_8x8x4(kx[1], Bx[1][v], d0, d1);
-        const double* Fy = sF + (1 * NV + v) * NPE;
-        dmma_8x8x4(Fy[r + N * c], ky[0], d0, d1);        // += F_y K_y^T, A = F_y[i=r][j=c]
-        dmma_8x8x4(Fy[r + N * (c + 4)], ky[1], d0, d1);  // A = F_y[i=r][j=c+4]
-        double dv[2] = {d0, d1};
+        double D = 0.0;
 #pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2) {
-          const int j = 2 * c + s2;
-          // lifted face fluxes, branch-free: x faces at i = 0 / N-1 (line j),
-          // y faces at j = 0 / N-1 (line i = r); interior nodes add 0 * (a face value)
-          dv[s2] = fma(xco, sH[(xf * NV + v) * L + j], dv[s2]);
-          dv[s2] = fma(yco[s2], sH[(yf[s2] * NV + v) * L + r], dv[s2]);
-          const size_t gi = ebase + (size_t)v * NPE + r + N * j;
-          const double kv = dv[s2] * dt;
-          if (!last) {
-            p.out[gi] = kv;
-          } else {
-            double S, Uu;
-            const int ln = v * NPE + r + N * j;
-            if (depth > 0)
-              combine_s<EXACT, NU, AM, BM>(p, src + ln, G::CHUNK, true, Uu, S);
-            else
-              combine_g<EXACT, NU, AM, BM>(p, ebase + ln, true, Uu, S);
-            un[s2][v] = fma(p.b_last, kv, S);
-            p.out[gi] = un[s2][v];
-          }
+        for (int d = 0; d < DIM; ++d) {
+          const int k = G::pos_of(d, n), t = G::line_of(d, n);
+          const double* Fl = sF + (d * NV + v) * NPE;
+          const double* Kr = &p.K[d][k * N];
+          // 0 + K0 F0 + K1 F1 + ...: the leading 0 + only normalises a -0,
+          // which zero_plus (axis 0) or the add onto dudt (axes > 0) reproduces
+          double acc = A::mul(Kr[0], Fl[G::node(d, t, 0)]);
+#pragma unroll
+          for (int l = 1; l < N; ++l) acc = A::mac(acc, Kr[l], Fl[G::node(d, t, l)]);
+          D = d == 0 ? zero_plus(acc) : A::add(D, acc);
+          if (k == 0) D = A::add(D, A::mul(p.lift[d], sH[((2 * d) * NV + v) * L + t]));
+          if (k == N - 1) D = A::sub(D, A::mul(p.lift[d], sH[((2 * d + 1) * NV + v) * L + t]));
+        }
+        const size_t gi = ebase + (size_t)v * NPE + n;
+        const double kv = A::mul(D, dt);  // k_i *= dt (solver.hpp:66-67)
+        if (!last) {
+          p.out[gi] = kv;
+        } else {
+          un[v] = p.b_last != 0.0 ? A::mac(Sn[m][v], p.b_last, kv) : Sn[m][v];
+          p.out[gi] = un[v];
         }
       }
       if (last) {
+        bool fin = true;
 #pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2) {
-          double sum = un[s2][0];  // non-finite iff some component is
-#pragma unroll
-          for (int v = 1; v < NV; ++v) sum += un[s2][v];
-          if (!isfinite(sum)) record_error(ctl, error_key(step, kPhaseInstability, 0, 0));
-          if (KIND == 1 && p.scan_alpha) {
-            const int n = r + N * (2 * c + s2);
-            if (!(un[s2][0] > 0.0)) {
-              record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(), G::aos_node(n)));
-            } else {
-              double mm = 0.0;
-#pragma unroll
-              for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[s2][1 + d]));
-              alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[s2][0]), p.sound_speed));  // == alpha_scan_kernel
-            }
-          }
-        }
-      }
-    } else {
-#pragma unroll
-      for (int m = 0; m < G::NM; ++m) {
-        const int n = lane + 32 * m;
-        if (n >= NPE) continue;
-        double un[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double D = 0.0;
-#pragma unroll
-          for (int d = 0; d < DIM; ++d) {
-            const int k = G::pos_of(d, n), t = G::line_of(d, n);
-            const double* Fl = sF + (d * NV + v) * NPE;
-            const double* Kr = &p.K[d][k * N];
-            // 0 + K0 F0 + K1 F1 + ...: the leading 0 + only normalises a -0,
-            // which zero_plus (axis 0) or the add onto dudt (axes > 0) reproduces
-            double acc = A::mul(Kr[0], Fl[G::node(d, t, 0)]);
-#pragma unroll
-            for (int l = 1; l < N; ++l) acc = A::mac(acc, Kr[l], Fl[G::node(d, t, l)]);
-            D = d == 0 ? zero_plus(acc) : A::add(D, acc);
-            if (k == 0) D = A::add(D, A::mul(p.lift[d], sH[((2 * d) * NV + v) * L + t]));
-            if (k == N - 1) D = A::sub(D, A::mul(p.lift[d], sH[((2 * d + 1) * NV + v) * L + t]));
-          }
-          const size_t gi = ebase + (size_t)v * NPE + n;
-          const double kv = A::mul(D, dt);  // k_i *= dt (solver.hpp:66-67)
-          if (!last) {
-            p.out[gi] = kv;
+        for (int v = 0; v < NV; ++v) fin = fin && isfinite(un[v]);
+        if (!fin) record_error(ctl, error_key(step, kPhaseInstability, 0, 0));
+        if (KIND == 1 && p.scan_alpha) {
+          if (!(un[0] > 0.0)) {
+            record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(), G::aos_node(n)));
           } else {
-            un[v] = p.b_last != 0.0 ? A::mac(Sn[m][v], p.b_last, kv) : Sn[m][v];
-            p.out[gi] = un[v];
-          }
-        }
-        if (last) {
-          bool fin = true;
+            double mm = 0.0;
 #pragma unroll
-          for (int v = 0; v < NV; ++v) fin = fin && isfinite(un[v]);
-          if (!fin) record_error(ctl, error_key(step, kPhaseInstability, 0, 0));
-          if (KIND == 1 && p.scan_alpha) {
-            if (!(un[0] > 0.0)) {
-              record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(), G::aos_node(n)));
-            } else {
-              double mm = 0.0;
-#pragma unroll
-              for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[1 + d]));
-              alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[0]), p.sound_speed));
-            }
+            for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[1 + d]));
+            alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[0]), p.sound_speed));
           }
         }
       }
