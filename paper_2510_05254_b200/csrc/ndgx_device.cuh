@@ -50,6 +50,8 @@ __host__ __device__ inline unsigned long long error_key(long long step, int phas
 // Device-resident step control (advance, solver.cpp:405-436).
 struct Control {
   unsigned long long alpha_bits;  // running max wavespeed of the current state (>= 0)
+  unsigned long long any_err;     // 1 once any error was recorded; max-reduced with alpha_bits
+                                  // across ranks so every rank stops at the same step
   unsigned long long err_key;     // first error in reference execution order
   double dt;
   double t;
@@ -58,6 +60,7 @@ struct Control {
   long long steps;                // steps begun
   int skip;                       // current step inactive (done / error)
   int done;                       // t_end reached
+  int aborted;                    // multi-rank: some rank failed, this one stopped with it
 };
 
 struct StepParams {
@@ -68,6 +71,7 @@ struct StepParams {
   double two_n_minus_1;   // (2N - 1)
   double const_alpha;     // advection: max_d |a_d|; < 0 for Euler (scanned)
   int warmup;             // warm-up step: non-finite dt -> t_end, no stats
+  int ranked;             // multi-rank solver: any_err (all-reduced) stops every rank
 };
 
 // Stage signatures of the supported tableaus (make_rk3/4/6, solver.cpp:17-68):
@@ -184,6 +188,7 @@ __device__ __forceinline__ void lax_friedrichs(const double* um, const double* u
 
 __device__ __forceinline__ void record_error(Control* ctl, unsigned long long key) {
   if (key < *(volatile unsigned long long*)&ctl->err_key) atomicMin(&ctl->err_key, key);
+  if (*(volatile unsigned long long*)&ctl->any_err == 0ull) atomicMax(&ctl->any_err, 1ull);
 }
 
 __device__ __forceinline__ double warp_max(double v) {
@@ -250,7 +255,15 @@ __global__ void alpha_scan_kernel(const double* __restrict__ u, int c0, int c1, 
 // loop bookkeeping of advance (solver.cpp:407-436), without host round trips.
 static __global__ void step_begin_kernel(StepParams sp) {
   Control* c = sp.ctl;
-  if (c->err_key != kNoError || c->done) {
+  if (c->done) {
+    c->skip = 1;
+    return;
+  }
+  if (sp.ranked ? c->any_err != 0ull : c->err_key != kNoError) {
+    // a rank solver stops on the all-reduced flag, so every rank -- the
+    // failing one included -- stops at this same step (run_partitioned:
+    // "stopped by failure elsewhere", src/partition.cpp:239-241)
+    if (sp.ranked) c->aborted = 1;
     c->skip = 1;
     return;
   }

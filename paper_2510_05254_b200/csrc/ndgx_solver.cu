@@ -215,8 +215,9 @@ struct ndgx_solver {
   // Per step: every rank's dt comes from the global max wavespeed (the
   // alpha barrier of run_partitioned, src/partition.cpp:201-213, 243-252).
   void launch_alpha_reduce(Control* c) const {
-    if (!comm || kind != NDGX_EULER_ISOTHERMAL) return;
-    nccl_check(nc->AllReduce(&c->alpha_bits, &c->alpha_bits, 1, ncclUint64, ncclMax, comm, stream),
+    if (!comm) return;
+    // {alpha_bits, any_err}: the global wavespeed and whether any rank failed
+    nccl_check(nc->AllReduce(&c->alpha_bits, &c->alpha_bits, 2, ncclUint64, ncclMax, comm, stream),
                "ncclAllReduce");
   }
 
@@ -243,6 +244,7 @@ struct ndgx_solver {
     sp.two_n_minus_1 = two_n_minus_1;
     sp.const_alpha = const_alpha;
     sp.warmup = warmup;
+    sp.ranked = comm != nullptr ? 1 : 0;
     return sp;
   }
 
@@ -930,6 +932,12 @@ static int finish_run(ndgx_solver* s, long long fixed, int start_par, ndgx_stats
       return s->report(c.err_key, start_par, err);
     }
   }
+  if (c.aborted && c.err_key == ndgx::kNoError) {
+    s->parity = start_par;
+    set_error(err, NDGX_ERR_RUN, "rank " + std::to_string(s->plan.rank) + ": stopped by failure elsewhere");
+    if (err) err->worker = s->plan.rank;
+    return NDGX_ERR_RUN;
+  }
   s->parity = start_par ^ (int)(c.steps & 1);
   if (stats) {
     stats->steps = (long)c.steps;
@@ -973,7 +981,9 @@ int ndgx_advance(ndgx_solver* s, long fixed_steps, int warmup, ndgx_stats* stats
       for (;;) {
         for (int q = 0; q < chunk; ++q) ck(cudaGraphLaunch(s->graph[start_par], s->stream), "graph");
         const Control c = s->read_control(s->ctl);
-        if (c.done || c.err_key != ndgx::kNoError) break;
+        // a rank solver stops only when every rank does (done, or aborted after
+        // the all-reduced error flag), so no rank leaves collectives unmatched
+        if (c.done || (s->comm ? c.aborted != 0 : c.err_key != ndgx::kNoError)) break;
       }
     }
     return finish_run(s, fixed, start_par, stats, err);

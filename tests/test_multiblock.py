@@ -209,3 +209,26 @@ def test_nccl_self_exchange_fast_mode_and_t_end(nccl_id):
     (a, sa), (b, sb) = res
     assert sa.steps == sb.steps and sa.dt_min == sb.dt_min
     assert np.array_equal(a, b)  # same kernels, same arithmetic, same halos
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("plan", [ndgx.StepPlan(5, False), ndgx.StepPlan(-1, False)])
+def test_rank_solver_errors_match_the_single_block(plan):
+    """A PhysicsError through the transport path: same exception, same message,
+    in fixed-step and t_end mode (the stop decision is all-reduced, so a rank
+    never leaves collectives unmatched)."""
+    cfg = _cfg(2, (12, 10), 8, True)
+    cfg.t_end = 0.05
+    u0 = ndgx.init_euler_subsonic(cfg.mesh, cfg.model)
+    f = _field(u0.copy(), cfg, cfg.mesh.cells)
+    f[3, 2, 0, 1, 5, 0, 0] = -0.5  # a negative density in cell (3, 2)
+    bad = f.reshape(-1)
+    msgs = []
+    for ranked in (False, True):
+        s = ndgx.Solver.for_rank(cfg, 1, 0, ndgx.nccl_unique_id(), force_exchange=True) if ranked else ndgx.Solver(cfg)
+        with s:
+            s.upload(bad)
+            with pytest.raises(ndgx.PhysicsError) as ei:
+                s.advance(plan)
+            msgs.append(str(ei.value))
+    assert msgs[0] == msgs[1]
