@@ -371,8 +371,24 @@ def bench_ours(args):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+        if args.csv:
+            write_csv_row(args, cfg, st, t_dev, world, torch.cuda.get_device_name(dev))
     if world > 1:
         dist.destroy_process_group()
+
+
+def write_csv_row(args, cfg, st, wall, world, device):
+    """--csv: the device-timed run as one row of the reference's report
+    (report_to_csv, src/report.cpp:180-198; row = base_row + fill_stats,
+    src/experiments.cpp:50-75), wall_seconds = max over ranks."""
+    import paper_2510_05254_b200 as ndgx
+    from paper_2510_05254_b200 import report as rp
+    stats = ndgx.StepStats(st.steps, st.dt_min, st.dt_max, wall)
+    row = rp.timing_row(cfg, stats, world, f"{device} (ndgx {args.arith})", experiment="timing",
+                        note=f"bench.py --config {args.config}")
+    meta = rp.ReportMeta("ndgx-" + ndgx.version().split()[1], "", time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()))
+    with open(args.csv, "w") as f:
+        f.write(rp.report_to_csv(rp.BenchReport(meta, [row])))
 
 
 def main():
@@ -390,6 +406,7 @@ def main():
                          "instead of stacking N copies (weak scaling, the default)")
     ap.add_argument("--force-exchange", action="store_true",
                     help="run the multi-GPU rank path even at one rank (every axis through NCCL)")
+    ap.add_argument("--csv", default=None, help="also write the run as a reference-schema report CSV")
     args = ap.parse_args()
     if args.impl == "reference":
         bench_reference_arm(args)

@@ -47,6 +47,19 @@ def test_bench_contract_on_gpu():
 
 
 @pytest.mark.gpu
+def test_bench_csv_row_in_the_reference_schema(tmp_path):
+    from paper_2510_05254_b200 import report as rp
+    path = tmp_path / "bench.csv"
+    line = _run("--config", "c2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-exact-arm",
+                "--csv", str(path))
+    lines = path.read_text().splitlines()
+    assert lines[0] == "# ndg-bench report" and lines[2] == ",".join(rp.COLUMNS)
+    row = dict(zip(rp.COLUMNS, lines[3].split(",")))
+    assert row["experiment"] == "timing" and row["steps"] == "3" and row["rk"] == "rk4"
+    assert abs(float(row["wall_seconds"]) * 1e3 / 3 - line["ms_per_step"]) < 1e-9 * line["ms_per_step"]
+
+
+@pytest.mark.gpu
 def test_bench_multi_rank_path_at_one_rank():
     line = _run("--config", "c2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-exact-arm",
                 "--force-exchange")
