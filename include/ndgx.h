@@ -138,6 +138,13 @@ int ndgx_init_multisine(const ndgx_problem* p, const double* amplitudes, int n_m
 void ndgx_multisine_amplitudes(int n_modes, uint64_t seed, double* out);
 int ndgx_init_euler_subsonic(const ndgx_problem* p, double* u_aos);
 
+/* Host diagnostics, summed in the reference's order (bit-identical):
+ *   ndgx_l2_error         <- l2_error (src/grid.cpp:190-203), var in [0, nvar)
+ *   ndgx_conserved_totals <- conserved_totals (src/grid.cpp:205-213), out[nvar] */
+int ndgx_l2_error(const ndgx_problem* p, const double* a_aos, const double* b_aos, int var,
+                  double* out);
+int ndgx_conserved_totals(const ndgx_problem* p, const double* u_aos, double* out);
+
 /* Block decomposition (partition.cpp:44-106): grid[3]; lo/hi [workers][3];
  * nbr [workers][3][2] (low, high). */
 int ndgx_decompose(int dim, const int cells[3], int workers, int grid[3], int* lo, int* hi,

@@ -134,6 +134,13 @@ double ref_l2_error(const ndgo_config* c, const double* a, const double* b, int 
                        field_of(c, b), var);
 }
 
+int ref_conserved_totals(const ndgo_config* c, const double* u, double* out) {
+  const std::vector<double> t =
+      ndg::conserved_totals(mesh_of(c), ndg::gauss_lobatto(c->order), field_of(c, u));
+  std::memcpy(out, t.data(), t.size() * sizeof(double));
+  return 0;
+}
+
 int ref_serial_rhs(const ndgo_config* c, const double* u, double* dudt, ndgo_error* err) {
   return guarded(err, [&] {
     const ndg::Mesh mesh = mesh_of(c);

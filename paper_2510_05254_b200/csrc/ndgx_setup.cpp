@@ -138,7 +138,28 @@ void for_each_node_parallel(const ndgx_problem* p, Fn&& fn) {
   for (auto& t : th) t.join();
 }
 
-void node_coords(const ndgx_problem* p, const double* gl, const int cell[3], const int node[3],
+// for_each_node (src/grid.cpp:28-48), sequential, with its quadrature weight
+// jac * prod_a w[node_a] formed in the same order (for order-dependent sums).
+template <typename Fn>
+void for_each_node_weighted(const ndgx_problem* p, const double* w, Fn&& fn) {
+  int nc[3] = {1, 1, 1};
+  for (int a = 0; a < p->dim; ++a) nc[a] = p->order;
+  double jac = 1.0;
+  for (int a = 0; a < p->dim; ++a) jac *= 0.5 * cell_size(p, a);
+  int cell[3], node[3];
+  for (cell[0] = 0; cell[0] < cells_of(p, 0); ++cell[0])
+    for (cell[1] = 0; cell[1] < cells_of(p, 1); ++cell[1])
+      for (cell[2] = 0; cell[2] < cells_of(p, 2); ++cell[2])
+        for (node[0] = 0; node[0] < nc[0]; ++node[0])
+          for (node[1] = 0; node[1] < nc[1]; ++node[1])
+            for (node[2] = 0; node[2] < nc[2]; ++node[2]) {
+              double wt = jac;
+              for (int a = 0; a < p->dim; ++a) wt *= w[node[a]];
+              fn(cell, node, wt);
+            }
+}
+
+void node_coords(const ndgx_problem* p, const double* gl,const int cell[3], const int node[3],
                  double x[3]) {
   x[0] = x[1] = x[2] = 0.0;  // node_coordinates (src/grid.cpp:109-125)
   for (int a = 0; a < p->dim; ++a) {
@@ -354,6 +375,36 @@ int ndgx_init_euler_subsonic(const ndgx_problem* p, double* u) {
     u[aos_index(p, nv, cell, node, 1)] = rho * ux;
     u[aos_index(p, nv, cell, node, 2)] = rho * uy;
     if (p->dim == 3) u[aos_index(p, nv, cell, node, 3)] = 0.0;
+  });
+  return NDGX_OK;
+}
+
+// l2_error (src/grid.cpp:190-203): sequential in for_each_node order
+// (src/grid.cpp:28-48) with the same weight products, so the sum is the
+// reference's bit for bit.  Host diagnostics for the convergence experiments.
+int ndgx_l2_error(const ndgx_problem* p, const double* a, const double* b, int var, double* out) {
+  double gl[16], w[16];
+  if (!p || !a || !b || !out || ndgx_gauss_lobatto(p->order, gl, w)) return NDGX_ERR_CONFIG;
+  const int nv = p->equation == NDGX_ADVECTION ? 1 : p->dim + 1;
+  if (var < 0 || var >= nv) return NDGX_ERR_CONFIG;
+  double sum = 0.0;
+  for_each_node_weighted(p, w, [&](const int cell[3], const int node[3], double wt) {
+    const size_t i = aos_index(p, nv, cell, node, var);
+    const double d = a[i] - b[i];
+    sum += wt * d * d;
+  });
+  *out = std::sqrt(sum);
+  return NDGX_OK;
+}
+
+// conserved_totals (src/grid.cpp:205-213): out[nvar]
+int ndgx_conserved_totals(const ndgx_problem* p, const double* u, double* out) {
+  double gl[16], w[16];
+  if (!p || !u || !out || ndgx_gauss_lobatto(p->order, gl, w)) return NDGX_ERR_CONFIG;
+  const int nv = p->equation == NDGX_ADVECTION ? 1 : p->dim + 1;
+  for (int v = 0; v < nv; ++v) out[v] = 0.0;
+  for_each_node_weighted(p, w, [&](const int cell[3], const int node[3], double wt) {
+    for (int v = 0; v < nv; ++v) out[v] += wt * u[aos_index(p, nv, cell, node, v)];
   });
   return NDGX_OK;
 }

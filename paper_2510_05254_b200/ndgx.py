@@ -504,6 +504,33 @@ def init_euler_subsonic(mesh: Mesh, model: EquationModel, out: Optional[np.ndarr
     return out
 
 
+def l2_error(mesh: Mesh, model: EquationModel, a, b, var: int = 0) -> float:
+    """l2_error (src/grid.cpp:190-203), summed in the reference's order (bit-identical)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if a.size != mesh.dof(model) or b.size != a.size:
+        raise ConfigError("l2_error: field shapes do not match")
+    if not 0 <= var < model.n_var():
+        raise IndexError("l2_error: bad variable")
+    p = make_problem(SolverConfig(mesh, model))
+    out = C.c_double()
+    if lib().ndgx_l2_error(C.byref(p), _dptr(a), _dptr(b), var, C.byref(out)) != 0:
+        raise ConfigError("l2_error: invalid problem")
+    return out.value
+
+
+def conserved_totals(mesh: Mesh, model: EquationModel, u) -> np.ndarray:
+    """conserved_totals (src/grid.cpp:205-213), summed in the reference's order."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    if u.size != mesh.dof(model):
+        raise ConfigError("conserved_totals: field shape does not match")
+    p = make_problem(SolverConfig(mesh, model))
+    out = np.zeros(model.n_var())
+    if lib().ndgx_conserved_totals(C.byref(p), _dptr(u), _dptr(out)) != 0:
+        raise ConfigError("conserved_totals: invalid problem")
+    return out
+
+
 @dataclass
 class Block:
     coord: tuple

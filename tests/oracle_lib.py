@@ -160,6 +160,7 @@ class Oracle:
             L.ref_run_partitioned.argtypes = [cfg, P(C.c_double), C.c_int, C.c_long, C.c_int, P(NdgoStats), P(NdgoError)]
             L.ref_l2_error.restype = C.c_double
             L.ref_l2_error.argtypes = [cfg, P(C.c_double), P(C.c_double), C.c_int]
+            L.ref_conserved_totals.argtypes = [cfg, P(C.c_double), P(C.c_double)]
             L.ref_init_multisine.argtypes = [cfg, P(C.c_double), C.c_int, P(C.c_double)]
             L.ref_init_multisine_seed.argtypes = [cfg, C.c_int, C.c_ulonglong, P(C.c_double)]
             L.ref_init_euler_subsonic.argtypes = [cfg, P(C.c_double)]
@@ -237,6 +238,13 @@ class Oracle:
         b = np.ascontiguousarray(b, dtype=np.float64)
         fn = self.lib.ndgo_l2_error if self.kind == "port" else self.lib.ref_l2_error
         return fn(C.byref(p.ndgo()), _dp(a), _dp(b), var)
+
+    def conserved_totals(self, p: Problem, u: np.ndarray) -> np.ndarray:
+        assert self.kind == "reference"
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.zeros(p.n_var)
+        self.lib.ref_conserved_totals(C.byref(p.ndgo()), _dp(u), _dp(out))
+        return out
 
     def basis(self, order: int):
         nodes, w, d = np.zeros(order), np.zeros(order), np.zeros(order * order)
