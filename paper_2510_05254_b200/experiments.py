@@ -307,3 +307,43 @@ def run_experiment(spec: ExperimentSpec, runner: Optional[Runner] = None) -> Ben
                                if spec.experiment not in ("scale", "energy", "simulate") else
                                f"experiment '{spec.experiment}' is not on the GPU path (SURVEY.md §8)")
     return fns[spec.experiment](spec, runner)
+
+
+def main(argv=None) -> int:
+    """``python -m paper_2510_05254_b200.experiments <experiment> [options]``:
+    the sweep options of the reference's ndg-bench (tools/ndg_bench.cpp:72-98)
+    for the experiments on the GPU path; CSV reports only."""
+    import argparse
+    ap = argparse.ArgumentParser(prog="python -m paper_2510_05254_b200.experiments")
+    ap.add_argument("experiment", choices=["converge", "cost", "fit", "timing"])
+    ap.add_argument("--equation", default="advection")
+    ap.add_argument("--dim", type=int, default=1)
+    ap.add_argument("--order", type=int, action="append")
+    ap.add_argument("--rk", default="rk6")
+    ap.add_argument("--cells", type=int, action="append")
+    ap.add_argument("--nk", type=int, default=4)
+    ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--workers", type=int, action="append")
+    ap.add_argument("--cfl", type=float, default=0.4)
+    ap.add_argument("--t-end", type=float, default=1.0)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--compare-equations", action="store_true")
+    ap.add_argument("--arith", choices=["exact", "fast"], default="exact")
+    ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--out", default=None, help="report path (default: <experiment>.csv)")
+    a = ap.parse_args(argv)
+    if a.equation == "advection" and a.seed is None:
+        ap.error("--seed is required for experiments with random sine amplitudes")
+    if not a.cells:
+        ap.error("--cells is required (one value per run in the sweep)")
+    spec = ExperimentSpec(a.experiment, a.equation, a.dim, a.order or [4], a.rk, a.cells, a.nk, a.seed or 0,
+                          a.workers or [1], a.cfl, a.t_end, a.steps, compare_equations=a.compare_equations)
+    rep = run_experiment(spec, Runner(a.device, ndgx.ARITH_FAST if a.arith == "fast" else ndgx.ARITH_EXACT))
+    from .report import report_to_csv
+    with open(a.out or f"{a.experiment}.csv", "w") as f:
+        f.write(report_to_csv(rep))
+    return 1 if any(r.status == "failed" for r in rep.rows) else 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

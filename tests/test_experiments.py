@@ -178,3 +178,36 @@ def test_2d_order8_convergence_at_gpu_scale():
     errs = _errors(2, 8, "rk6", cells)
     slopes = _doubling_slopes(cells, errs)
     assert max(slopes) >= 7.5, (errs, slopes)
+
+
+@pytest.mark.gpu
+def test_c8_fit_constants_on_gpu():
+    """Criterion 8 (acceptance.cpp:340-394): dof * err^(1/order) at 1e-3 and
+    1e-4, orders 3..8, 1D RK6 sweeps: spread <= 3x, all within 3x of 200."""
+    sweeps = {3: [800, 1600, 2400], 4: [200, 400, 800], 5: [120, 240, 480], 6: [80, 160, 320],
+              7: [40, 60, 120], 8: [40, 50, 100]}
+    cs = []
+    for order, cells in sweeps.items():
+        spec = ex.ExperimentSpec("converge", "advection", 1, [order], "rk6", cells, 40, 42)
+        curve = [(float(c * order), r.l2_error) for c, r in
+                 zip(cells, [r for r in ex.run_converge(spec).rows if r.row_type == "run"])]
+        for target in (1e-3, 1e-4):
+            dof = ex.interpolate_dof_for_error(curve, target)
+            assert not math.isnan(dof), (order, target, curve)
+            cs.append(dof * target ** (1.0 / order))
+    assert max(cs) / min(cs) <= 3.0 and max(cs) <= 600.0 and min(cs) >= 200.0 / 3.0, cs
+
+
+def test_cli_writes_the_report(tmp_path, monkeypatch):
+    """The CLI builds the spec like ndg-bench; the runner is stubbed (no GPU)."""
+    seen = {}
+
+    def fake(spec, runner=None):
+        seen["spec"] = spec
+        return rp.BenchReport(rows=[rp.BenchRow(experiment=spec.experiment)])
+    monkeypatch.setattr(ex, "run_experiment", fake)
+    out = tmp_path / "r.csv"
+    assert ex.main(["converge", "--order", "4", "--order", "6", "--cells", "8", "--cells", "16", "--seed", "42",
+                    "--out", str(out)]) == 0
+    assert seen["spec"].orders == [4, 6] and seen["spec"].cells == [8, 16] and seen["spec"].seed == 42
+    assert out.read_text().startswith("# ndg-bench report\n")
