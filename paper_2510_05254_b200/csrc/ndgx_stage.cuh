@@ -527,7 +527,15 @@ struct Lane8 {
   double xco, yco0, yco1;  // face-lift coefficients of the output nodes
   int xf;                // x face (0 / 1) feeding the output row r
   double kx[2], ky[2];   // K_x[r][2c+h], K_y[r][2c+h] (k-step h pairs l = 2c + h)
+  int n0s, a0s, a1s;     // swizzled slab slots of n0 and of the A / output nodes o0, o0 + 8
 };
+
+// Slab slot of node n = i + 8 j for the flagship's F_y and S arrays: the
+// 16-byte unit n / 2 is XORed with 2 ((j / 2) mod 4).  The node-phase stores
+// (double2 at i = 2c, j = r) stay conflict-free and the transposed reads
+// (i = r, j = 2c or 2c + 1, by lanes 4r + c) hit eight distinct bank quads
+// per half-warp instead of two (a 4-way conflict unswizzled).
+__host__ __device__ constexpr int swz8(int n) { return n ^ (((n >> 4) & 3) << 2); }
 
 // Stages that read only u (stage 0, serial_rhs): the element's raw inputs
 // are loaded one element ahead (the lane's node pair and face-neighbour node),
@@ -620,7 +628,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       double S0, S1;
       combine_pair<NU, AM, BM>(p, ring, src + v * NPE + ln.n0, ebase + v * NPE + ln.n0, CHUNK, Up[0][v], Up[1][v],
                                &S0, &S1);
-      *reinterpret_cast<double2*>(sS + v * NPE + ln.n0) = make_double2(S0, S1);
+      *reinterpret_cast<double2*>(sS + v * NPE + ln.n0s) = make_double2(S0, S1);
     } else {
       combine_pair<NU, AM>(p, ring, src + v * NPE + ln.n0, ebase + v * NPE + ln.n0, CHUNK, Up[0][v], Up[1][v]);
     }
@@ -683,7 +691,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v)
-    *reinterpret_cast<double2*>(sF + v * NPE + ln.n0) = make_double2(Fyp[0][v], Fyp[1][v]);
+    *reinterpret_cast<double2*>(sF + v * NPE + ln.n0s) = make_double2(Fyp[0][v], Fyp[1][v]);
   __syncwarp();
 
   // ---------------------------------------------------------- faces
@@ -744,8 +752,8 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
     dmma_8x8x4(ln.kx[0], Bx[0][v], d0, d1);  // D_x = K_x F_x
     dmma_8x8x4(ln.kx[1], Bx[1][v], d0, d1);
     const double* Fy = sF + v * NPE;
-    dmma_8x8x4(Fy[ln.r + N * (2 * ln.c)], ln.ky[0], d0, d1);  // += F_y K_y^T, A = F_y[i=r][j=2c+h]
-    dmma_8x8x4(Fy[ln.r + N * (2 * ln.c + 1)], ln.ky[1], d0, d1);
+    dmma_8x8x4(Fy[ln.a0s], ln.ky[0], d0, d1);  // += F_y K_y^T, A = F_y[i=r][j=2c+h]
+    dmma_8x8x4(Fy[ln.a1s], ln.ky[1], d0, d1);
     // lifted face fluxes: x faces on rows r = 0 / 7 (line j), y faces on
     // columns j = 0 (s = 0 of c = 0) / 7 (s = 1 of c = 3) (line i = r)
     const double* hx = sH + (ln.xf * NV + v) * L + 2 * ln.c;
@@ -758,7 +766,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       gout[v * NPE + ln.o0] = k0;
       gout[v * NPE + ln.o0 + 8] = k1;
     } else {
-      const double S0 = sS[v * NPE + ln.o0], S1 = sS[v * NPE + ln.o0 + 8];
+      const double S0 = sS[v * NPE + ln.a0s], S1 = sS[v * NPE + ln.a1s];
       un[0][v] = fma(p.b_last, k0, S0);
       un[1][v] = fma(p.b_last, k1, S1);
       gout[v * NPE + ln.o0] = un[0][v];
@@ -901,6 +909,9 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     // the neighbour's facing node: x-lo (7, t), x-hi (0, t), y-lo (t, 7), y-hi (t, 0)
     ln8.nb_node = ln8.f == 0 ? 7 + 8 * ln8.t : (ln8.f == 1 ? 8 * ln8.t : (ln8.f == 2 ? ln8.t + 56 : ln8.t));
     ln8.o0 = r + 16 * c;
+    ln8.n0s = swz8(ln8.n0);
+    ln8.a0s = swz8(ln8.o0);
+    ln8.a1s = swz8(ln8.o0 + 8);
     ln8.xco = r == 0 ? p.lift[0] : (r == N - 1 ? -p.lift[0] : 0.0);
     ln8.xf = r == N - 1 ? 1 : 0;
     ln8.yco0 = c == 0 ? p.lift[1] : 0.0;
