@@ -44,7 +44,7 @@ StageKernel make_stage_kernel() {
   k.threads = G::THREADS;
   k.warps = G::WARPS;
   for (int q = 0; q < kNumSigs; ++q)
-    k.smem_fixed[q] = G::smem_bytes(0, 0, G::mma_body(EXACT, kSigs[q].nu), kSigs[q].bm != 0);
+    k.smem_fixed[q] = G::smem_bytes(0, 0, G::mma_body(EXACT, q), kSigs[q].bm != 0);
   k.ring_per_array = G::WARPS * G::SLOT1 * 8;
   k.tma_ok = G::TMA_OK;
   // Euler stages: 16 warps/SM of 16-byte direct loads keep more bytes in flight

@@ -41,6 +41,15 @@
 
 namespace ndgx {
 
+// Stage signatures (kSigs index) that take the 3D order-4 tensor-core body,
+// as measured at 128^3 cells: the u-only and one-term stages and the last
+// stage of every integrator (RK3 9.11 -> 8.92 ms, RK4 10.74 -> 9.16, RK6
+// 16.06 -> 13.97); the generic body stays faster for the intermediate RK6
+// stages with 2..5 terms (8.97 vs 9.17 ms at two terms, 14.4 vs 26.1 at five).
+#ifndef NDGX_MMA3_SIGS
+#define NDGX_MMA3_SIGS 0x10F
+#endif
+
 template <int DIM, int N, int KIND>
 struct Geo {
   static constexpr int NV = (KIND == 0) ? 1 : DIM + 1;
@@ -80,10 +89,9 @@ struct Geo {
                : WSLAB;
   }
   // which body a (arith, signature) kernel runs: the 2D N=8 / 3D N=4
-  // tensor-core bodies (contracted mode; 3D only for stages reading <= 1
-  // K_j -- the RK6 stages with more terms keep the generic body, measured)
-  static constexpr __host__ __device__ bool mma_body(bool exact, int nu) {
-    return !exact && (MMA || (MMA3 && nu <= 1));
+  // tensor-core bodies (contracted mode; 3D for the NDGX_MMA3_SIGS stages)
+  static constexpr __host__ __device__ bool mma_body(bool exact, int sig) {
+    return !exact && (MMA || (MMA3 && ((NDGX_MMA3_SIGS >> sig) & 1) != 0));
   }
   static constexpr int smem_bytes(int nu, int depth, bool mma, bool last) {
     return (HEAD + WARPS * (wslab(mma, last) + depth * (1 + nu) * SLOT1)) * 8;
@@ -294,6 +302,11 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
   const double a2 = KIND == 1 ? p.sound_speed : 0.0;
   const int r = lane >> 2, c = lane & 3;
   double* sS = sF + 3 * NV * NPE;  // last stage: S at the nodes
+  // XOR-swizzled slab slots (pairs n, n + 1 stay adjacent): F_x / running
+  // dudt / S with bits 3, 4 folded into bits 2, 3 (the accumulator patterns of
+  // axes 0 and 2 lose their 2- and 4-way conflicts), F_z with the z plane
+  // folded into bits 2, 3 (the B-operand reads of axis 2: 4-way -> none)
+  auto sw = [](int d, int n) { return d == 0 ? n ^ ((n >> 1) & 12) : (d == 2 ? n ^ (((n >> 4) & 3) << 2) : n); };
 
   // flux of U along axis d and the one-sided speed (models.cpp:42-70), contracted
   auto fluxd = [&](const double* U, int d, double* F, double& sp) {
@@ -340,7 +353,7 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
             s0 = fma(p.cb[t], k[1 + t].x, s0);
             s1 = fma(p.cb[t], k[1 + t].y, s1);
           }
-        *reinterpret_cast<double2*>(sS + v * NPE + n0) = make_double2(s0, s1);
+        *reinterpret_cast<double2*>(sS + v * NPE + sw(0, n0)) = make_double2(s0, s1);
       }
     }
     double Fp[DIM][2][NV];
@@ -370,7 +383,7 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
     for (int d = 0; d < DIM; ++d)
 #pragma unroll
       for (int v = 0; v < NV; ++v)
-        *reinterpret_cast<double2*>(sF + (d * NV + v) * NPE + n0) = make_double2(Fp[d][0][v], Fp[d][1][v]);
+        *reinterpret_cast<double2*>(sF + (d * NV + v) * NPE + sw(d, n0)) = make_double2(Fp[d][0][v], Fp[d][1][v]);
   }
   __syncwarp();
 
@@ -441,18 +454,19 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
         const int o0 = G::node(d, 8 * g + 2 * c, r), o1 = G::node(d, 8 * g + 2 * c + 1, r);
+        const int q0 = sw(0, o0), q1 = sw(0, o1);  // their accumulator slots
         double c0 = 0.0, c1 = 0.0;
         if (d > 0 && krow) {
-          c0 = acc[v * NPE + o0];
-          c1 = acc[v * NPE + o1];
+          c0 = acc[v * NPE + q0];
+          c1 = acc[v * NPE + q1];
         }
-        const double b = sF[(d * NV + v) * NPE + G::node(d, 8 * g + r, c)];
+        const double b = sF[(d * NV + v) * NPE + sw(d, G::node(d, 8 * g + r, c))];
         dmma_8x8x4(ln.k[d], b, c0, c1);
         if (d < DIM - 1) {
           __syncwarp();  // B/C reads of this group precede the in-place stores
           if (krow) {
-            acc[v * NPE + o0] = c0;
-            acc[v * NPE + o1] = c1;
+            acc[v * NPE + q0] = c0;
+            acc[v * NPE + q1] = c1;
           }
         } else if (krow) {
           // final axis: outputs at nodes o0, o0 + 1 = line + 16 r; lifted faces
@@ -473,11 +487,11 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
           if (!LAST) {
             *reinterpret_cast<double2*>(gout) = make_double2(k0, k1);
           } else {
-            const double u0 = fma(p.b_last, k0, sS[v * NPE + o0]);
-            const double u1 = fma(p.b_last, k1, sS[v * NPE + o1]);
+            const double u0 = fma(p.b_last, k0, sS[v * NPE + q0]);
+            const double u1 = fma(p.b_last, k1, sS[v * NPE + q1]);
             *reinterpret_cast<double2*>(gout) = make_double2(u0, u1);
-            acc[v * NPE + o0] = u0;  // u_new for the finite check / next alpha
-            acc[v * NPE + o1] = u1;
+            acc[v * NPE + q0] = u0;  // u_new for the finite check / next alpha
+            acc[v * NPE + q1] = u1;
           }
         }
       }
@@ -491,7 +505,7 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
       const int n = 2 * lane + h;
       double un[NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) un[v] = acc[v * NPE + n];
+      for (int v = 0; v < NV; ++v) un[v] = acc[v * NPE + sw(0, n)];
       double sum = un[0];
 #pragma unroll
       for (int v = 1; v < NV; ++v) sum += un[v];
@@ -813,7 +827,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   using A = Ar<EXACT>;
   constexpr int NV = G::NV, L = G::L, NPE = G::NPE, HW = G::HW;
   constexpr bool USE_MMA = G::MMA && !EXACT;
-  constexpr bool USE_MMA3 = G::MMA3 && G::mma_body(EXACT, kSigs[SIG].nu);
+  constexpr bool USE_MMA3 = G::MMA3 && G::mma_body(EXACT, SIG);
   constexpr int NU = kSigs[SIG].nu, AM = kSigs[SIG].am, BM = kSigs[SIG].bm;
   extern __shared__ __align__(16) double smem[];
 
