@@ -598,6 +598,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   const int C0 = p.cells[0], C1 = p.cells[1];
   const size_t ebase = (size_t)e * CHUNK;
   const double a2 = KIND == 1 ? p.sound_speed : 0.0;
+  constexpr bool FULL_TRACE = PRE || NU == 0;  // face traces with flux and speed
 
   // face neighbour loads first, so they are in flight together with the
   // node loads (one memory latency per element instead of two)
@@ -682,25 +683,28 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       Bx[h][v] = Fx[v];
       Fyp[h][v] = Fy[v];
     }
-    // face traces: x faces at i = 2c + h = 0 / 7, y faces at j = r = 0 / 7
+    // face traces: x faces at i = 2c + h = 0 / 7, y faces at j = r = 0 / 7.
+    // U only (the face lane recomputes flux and speed, cheaper than the
+    // shared-memory wavefronts of storing them), except in the u-only stage
+    // kernels, which measured 1.7x slower that way
     const int i = 2 * ln.c + h;
     if (i == 0 || i == N - 1) {
       double* t = sT + (i == 0 ? 0 : HW) * L + ln.r;
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         t[v * L] = U[v];
-        t[(NV + v) * L] = Fx[v];
+        if (FULL_TRACE) t[(NV + v) * L] = Fx[v];
       }
-      t[2 * NV * L] = sx;
+      if (FULL_TRACE) t[2 * NV * L] = sx;
     }
     if (ln.r == 0 || ln.r == N - 1) {
       double* t = sT + ((ln.r == 0 ? 2 : 3) * HW) * L + i;
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         t[v * L] = U[v];
-        t[(NV + v) * L] = Fy[v];
+        if (FULL_TRACE) t[(NV + v) * L] = Fy[v];
       }
-      t[2 * NV * L] = sy;
+      if (FULL_TRACE) t[2 * NV * L] = sy;
     }
   }
 #pragma unroll
@@ -729,30 +733,48 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
           if ((AM >> a & 1) != 0) Un[v] = fma(p.ca[a], Nraw[1 + a][v], Un[v]);
       }
     }
-    double Fn[NV], sn;
-    if (KIND == 0) {
-      Fn[0] = p.vel[d] * Un[0];
-      sn = fabs(p.vel[d]);
-    } else {
-      const double rinv = fast_rcp(Un[0]);
-      const double md = d == 0 ? Un[1] : Un[2];  // a select, not a (local-memory) dynamic index
-      const double ua = md * rinv;
-      const double pr = Un[0] * a2 * a2;
-      Fn[0] = md;
-      Fn[1] = d == 0 ? fma(ua, Un[1], pr) : ua * Un[1];
-      Fn[2] = d == 0 ? ua * Un[2] : fma(ua, Un[2], pr);
-      sn = fabs(ua) + a2;
-    }
+    // flux along d and one-sided speed (models.cpp:42-70), the node phase's expressions
+    auto fluxd = [&](const double* W, double* F, double& sp) {
+      if (KIND == 0) {
+        F[0] = p.vel[d] * W[0];
+        sp = fabs(p.vel[d]);
+      } else {
+        const double rinv = fast_rcp(W[0]);
+        const double md = d == 0 ? W[1] : W[2];  // a select, not a (local-memory) dynamic index
+        const double ua = md * rinv;
+        const double pr = W[0] * a2 * a2;
+        F[0] = md;
+        F[1] = d == 0 ? fma(ua, W[1], pr) : ua * W[1];
+        F[2] = d == 0 ? ua * W[2] : fma(ua, W[2], pr);
+        sp = fabs(ua) + a2;
+      }
+    };
     const double* own = sT + (f * HW) * L + ln.t;
-    const double so = own[2 * NV * L];
-    const double al = dmax(so, sn);
+    double Fn[NV], sn;
+    fluxd(Un, Fn, sn);
+    if constexpr (FULL_TRACE) {  // the traces carry flux and speed
+      const double so = own[2 * NV * L];
+      const double al = dmax(so, sn);
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
-      const double uo = own[v * L], fo = own[(NV + v) * L];
-      const double um = side ? uo : Un[v], up = side ? Un[v] : uo;
-      const double fm = side ? fo : Fn[v], fp = side ? Fn[v] : fo;
-      sH[(f * NV + v) * L + ln.t] = 0.5 * ((fm + fp) - al * (up - um));
+      for (int v = 0; v < NV; ++v) {
+        // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
+        const double uo = own[v * L], fo = own[(NV + v) * L];
+        const double um = side ? uo : Un[v], up = side ? Un[v] : uo;
+        const double fm = side ? fo : Fn[v], fp = side ? Fn[v] : fo;
+        sH[(f * NV + v) * L + ln.t] = 0.5 * ((fm + fp) - al * (up - um));
+      }
+    } else {
+      double Uo[NV], Fo[NV], so;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Uo[v] = own[v * L];
+      fluxd(Uo, Fo, so);
+      const double al = dmax(so, sn);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double um = side ? Uo[v] : Un[v], up = side ? Un[v] : Uo[v];
+        const double fm = side ? Fo[v] : Fn[v], fp = side ? Fn[v] : Fo[v];
+        sH[(f * NV + v) * L + ln.t] = 0.5 * ((fm + fp) - al * (up - um));
+      }
     }
   }
   __syncwarp();
