@@ -551,45 +551,11 @@ struct Lane8 {
 // per half-warp instead of two (a 4-way conflict unswizzled).
 __host__ __device__ constexpr int swz8(int n) { return n ^ (((n >> 4) & 3) << 2); }
 
-// Stages that read only u (stage 0, serial_rhs): the element's raw inputs
-// are loaded one element ahead (the lane's node pair and face-neighbour node),
-// so each warp keeps two elements' loads in flight.
-template <int NV>
-struct Pre0 {
-  double2 node[NV];
-  double face[NV];
-};
-
-template <int NV>
-__device__ __forceinline__ void load_pre0(const StageArgs& p, const Lane8& ln, int e, int cx, int cy, Pre0<NV>& pr) {
-  constexpr int NPE = 64, L = 8, CHUNK = NV * NPE;
-  const int C0 = p.cells[0], C1 = p.cells[1];
-  const int f = ln.f, d = f >> 1, side = f & 1;
-  const bool bnd = d == 0 ? (side ? cx == C0 - 1 : cx == 0) : (side ? cy == C1 - 1 : cy == 0);
-  const double* ext = p.ext[d][side];
-  if (bnd && ext != nullptr) {
-    const size_t xs = d == 0 ? (size_t)cy : (size_t)cx;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) pr.face[v] = __ldg(ext + (xs * NV + v) * L + ln.t);
-  } else {
-    const int step_d = d == 0 ? 1 : C0;
-    const int span = d == 0 ? C0 : C1;
-    const int en = side ? (bnd ? e - (span - 1) * step_d : e + step_d) : (bnd ? e + (span - 1) * step_d : e - step_d);
-    const size_t g = (size_t)en * CHUNK + ln.nb_node;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) pr.face[v] = __ldg(p.u + g + v * NPE);
-  }
-  const size_t nb = (size_t)e * CHUNK + ln.n0;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) pr.node[v] = __ldg(reinterpret_cast<const double2*>(p.u + nb + v * NPE));
-}
-
-template <int KIND, int NU, int AM, int BM, bool PRE = false>
+template <int KIND, int NU, int AM, int BM>
 __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8& ln, int lane, int e, int cx,
                                                  int cy, const double* src, const double* fsrc, bool ring,
                                                  double* sF, double* sT, double* sH, double dt, bool last,
-                                                 long long step, double& alpha,
-                                                 const Pre0<(KIND == 0 ? 1 : 3)>* pre = nullptr) {
+                                                 long long step, double& alpha) {
   constexpr int N = 8, NPE = 64, L = 8;
   constexpr int NV = KIND == 0 ? 1 : 3;
   constexpr int HW = 2 * NV + 1;
@@ -598,7 +564,6 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   const int C0 = p.cells[0], C1 = p.cells[1];
   const size_t ebase = (size_t)e * CHUNK;
   const double a2 = KIND == 1 ? p.sound_speed : 0.0;
-  constexpr bool FULL_TRACE = PRE || NU == 0;  // face traces with flux and speed
 
   // face neighbour loads first, so they are in flight together with the
   // node loads (one memory latency per element instead of two)
@@ -607,10 +572,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   const double* ext = p.ext[d][side];
   const bool from_ext = bnd && ext != nullptr;
   double Nraw[1 + NU][NV];
-  if (PRE) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) Nraw[0][v] = pre->face[v];
-  } else if (!ring) {
+  if (!ring) {
     if (from_ext) {
       const size_t xs = d == 0 ? (size_t)cy : (size_t)cx;
 #pragma unroll
@@ -636,10 +598,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   double* sS = sF + NV * NPE;  // last stage: S at the flux nodes, read back at the output nodes
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    if (PRE) {
-      Up[0][v] = pre->node[v].x;
-      Up[1][v] = pre->node[v].y;
-    } else if (last) {
+    if (last) {
       double S0, S1;
       combine_pair<NU, AM, BM>(p, ring, src + v * NPE + ln.n0, ebase + v * NPE + ln.n0, CHUNK, Up[0][v], Up[1][v],
                                &S0, &S1);
@@ -683,28 +642,19 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       Bx[h][v] = Fx[v];
       Fyp[h][v] = Fy[v];
     }
-    // face traces: x faces at i = 2c + h = 0 / 7, y faces at j = r = 0 / 7.
-    // U only (the face lane recomputes flux and speed, cheaper than the
-    // shared-memory wavefronts of storing them), except in the u-only stage
-    // kernels, which measured 1.7x slower that way
+    // face traces, U only (the face lane recomputes flux and speed, cheaper
+    // than the partial-warp shared stores of keeping them): x faces at
+    // i = 2c + h = 0 / 7, y faces at j = r = 0 / 7
     const int i = 2 * ln.c + h;
     if (i == 0 || i == N - 1) {
       double* t = sT + (i == 0 ? 0 : HW) * L + ln.r;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        t[v * L] = U[v];
-        if (FULL_TRACE) t[(NV + v) * L] = Fx[v];
-      }
-      if (FULL_TRACE) t[2 * NV * L] = sx;
+      for (int v = 0; v < NV; ++v) t[v * L] = U[v];
     }
     if (ln.r == 0 || ln.r == N - 1) {
       double* t = sT + ((ln.r == 0 ? 2 : 3) * HW) * L + i;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        t[v * L] = U[v];
-        if (FULL_TRACE) t[(NV + v) * L] = Fy[v];
-      }
-      if (FULL_TRACE) t[2 * NV * L] = sy;
+      for (int v = 0; v < NV; ++v) t[v * L] = U[v];
     }
   }
 #pragma unroll
@@ -752,25 +702,15 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
     const double* own = sT + (f * HW) * L + ln.t;
     double Fn[NV], sn;
     fluxd(Un, Fn, sn);
-    if constexpr (FULL_TRACE) {  // the traces carry flux and speed
-      const double so = own[2 * NV * L];
-      const double al = dmax(so, sn);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
-        const double uo = own[v * L], fo = own[(NV + v) * L];
-        const double um = side ? uo : Un[v], up = side ? Un[v] : uo;
-        const double fm = side ? fo : Fn[v], fp = side ? Fn[v] : fo;
-        sH[(f * NV + v) * L + ln.t] = 0.5 * ((fm + fp) - al * (up - um));
-      }
-    } else {
-      double Uo[NV], Fo[NV], so;
+    {
+      double Uo[NV], Fo[NV], so;  // this element's side, from its U trace
 #pragma unroll
       for (int v = 0; v < NV; ++v) Uo[v] = own[v * L];
       fluxd(Uo, Fo, so);
       const double al = dmax(so, sn);
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
+        // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
         const double um = side ? Uo[v] : Un[v], up = side ? Un[v] : Uo[v];
         const double fm = side ? Fo[v] : Fn[v], fp = side ? Fn[v] : Fo[v];
         sH[(f * NV + v) * L + ln.t] = 0.5 * ((fm + fp) - al * (up - um));
@@ -983,9 +923,6 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   }
   int slot = 0;
   uint32_t parity = 0;
-  [[maybe_unused]] Pre0<NV> pre0;
-  if constexpr (USE_MMA && NU == 0)
-    if (depth == 0 && e < nelem) load_pre0<NV>(p, ln8, e, cx, cy, pre0);
   for (; e < nelem; e += nw) {
     const size_t ebase = (size_t)e * NV * NPE;
     const double* src = ring + slot * SLOT;  // this element's u and K_j (when depth > 0)
@@ -1012,21 +949,6 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       element_3d4_fast<KIND, NU, AM, BM>(p, ln4, lane, e, cx, cy, cz, sF, sT, sH, dt, step, alpha);
       step_coords(cx, cy, cz);
       continue;
-    }
-    if constexpr (USE_MMA && NU == 0) {
-      if (depth == 0) {
-        Pre0<NV> nxt;
-        if (e + nw < nelem) {
-          int nx = cx, ny = cy, nz = cz;
-          step_coords(nx, ny, nz);
-          load_pre0<NV>(p, ln8, e + nw, nx, ny, nxt);
-        }
-        element_2d8_fast<KIND, NU, AM, BM, true>(p, ln8, lane, e, cx, cy, src, fsrc, false, sF, sT, sH, dt, last,
-                                                 step, alpha, &pre0);
-        pre0 = nxt;
-        step_coords(cx, cy, cz);
-        continue;
-      }
     }
     if constexpr (USE_MMA) {
       element_2d8_fast<KIND, NU, AM, BM>(p, ln8, lane, e, cx, cy, src, fsrc, depth > 0, sF, sT, sH, dt, last, step,
