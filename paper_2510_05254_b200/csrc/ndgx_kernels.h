@@ -50,7 +50,8 @@ StageKernel make_stage_kernel() {
   // Euler stages: 16 warps/SM of 16-byte direct loads keep more bytes in flight
   // than a per-warp TMA ring, whose shared memory costs resident warps
   // (C3 fast 3.22 vs 4.21 ms/step, exact 6.70 vs 6.8; profiles/README.md)
-  k.prefer_direct = KIND == 1 || G::MMA3;
+  // (the contracted 2D order-8 body too for advection: C2 0.284 vs 0.322 ms/step)
+  k.prefer_direct = KIND == 1 || G::MMA3 || (G::MMA && !EXACT);
   return k;
 }
 
