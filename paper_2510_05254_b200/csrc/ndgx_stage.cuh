@@ -791,6 +791,12 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   constexpr bool USE_MMA = G::MMA && !EXACT;
   constexpr bool USE_MMA3 = G::MMA3 && G::mma_body(EXACT, SIG);
   constexpr int NU = kSigs[SIG].nu, AM = kSigs[SIG].am, BM = kSigs[SIG].bm;
+#ifndef NDGX_GEN_UTRACE
+#define NDGX_GEN_UTRACE 1
+#endif
+  // generic body: face traces hold U only; the face lane recomputes its own
+  // side's flux and speed (fewer partial-warp shared stores)
+  constexpr bool GEN_UTRACE = NDGX_GEN_UTRACE != 0;
   extern __shared__ __align__(16) double smem[];
 
   Control* ctl = p.ctl;
@@ -1001,9 +1007,9 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
             t[v * L] = U[v];
-            t[(NV + v) * L] = F[v];
+            if (!GEN_UTRACE) t[(NV + v) * L] = F[v];
           }
-          t[2 * NV * L] = sp;
+          if (!GEN_UTRACE) t[2 * NV * L] = sp;
         }
       }
     }
@@ -1049,13 +1055,24 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       }
       double Fn[NV], sn;
       flux<DIM, KIND, EXACT>(p, Un, d, Fn, sn, (!EXACT && KIND == 1) ? fast_rcp(Un[0]) : -1.0);
-      const double so = own[2 * NV * L];
+      // this element's side: U from the trace, flux and speed recomputed
+      // (the same function of the same U as in the node phase)
+      double Uo[NV], Fo[NV], so;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Uo[v] = own[v * L];
+      if (GEN_UTRACE) {
+        flux<DIM, KIND, EXACT>(p, Uo, d, Fo, so, (!EXACT && KIND == 1) ? fast_rcp(Uo[0]) : -1.0);
+      } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) Fo[v] = own[(NV + v) * L];
+        so = own[2 * NV * L];
+      }
       const double a = dmax(side ? so : sn, side ? sn : so);
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
-        const double um = side ? own[v * L] : Un[v], up = side ? Un[v] : own[v * L];
-        const double fm = side ? own[(NV + v) * L] : Fn[v], fp = side ? Fn[v] : own[(NV + v) * L];
+        const double um = side ? Uo[v] : Un[v], up = side ? Un[v] : Uo[v];
+        const double fm = side ? Fo[v] : Fn[v], fp = side ? Fn[v] : Fo[v];
         sH[(f * NV + v) * L + t] = A::mul(0.5, A::sub(A::add(fm, fp), A::mul(a, A::sub(up, um))));
       }
     }
