@@ -293,7 +293,7 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
                                                  long long step, double& alpha) {
   constexpr int N = 4, NPE = 64, L = 16, DIM = 3;
   constexpr int NV = KIND == 0 ? 1 : 4;
-  constexpr int TW = NV + 1;  // trace record: U, one-sided speed
+  constexpr int TW = NV + 1;  // trace record: U (+1 spare slot); flux and speed are recomputed at the face
   constexpr int CHUNK = NV * NPE;
   constexpr bool LAST = BM != 0;
   using G = Geo<3, 4, KIND>;
@@ -375,7 +375,6 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
           double* t = sT + ((2 * d + (pos == 0 ? 0 : 1)) * TW) * L + G::line_of(d, n);
 #pragma unroll
           for (int v = 0; v < NV; ++v) t[v * L] = Up[h][v];
-          t[NV * L] = sp;
         }
       }
     }
@@ -428,9 +427,8 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
     const double* tr = sT + (f * TW) * L + t;
 #pragma unroll
     for (int v = 0; v < NV; ++v) Uo[v] = tr[v * L];
-    const double so = tr[NV * L];
-    double Fo[NV], Fn[NV], sn, dummy;
-    fluxd(Uo, d, Fo, dummy);
+    double Fo[NV], Fn[NV], so, sn;  // own side recomputed from its U trace
+    fluxd(Uo, d, Fo, so);
     fluxd(Un, d, Fn, sn);
     const double al = dmax(so, sn);
 #pragma unroll
