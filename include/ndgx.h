@@ -14,6 +14,9 @@
  *   ndgx_advance              <- advance (src/solver.cpp:372-440) with StepPlan
  *                                (include/ndg/solver.hpp:168-171), StepStats (:153-158)
  *   ndgx_decompose            <- decompose (src/partition.cpp:44-106)
+ *   ndgx_create_partitioned   <- run_partitioned (src/partition.cpp:186-333) as one
+ *                                handle over P blocks on 1..8 devices
+ *   ndgx_create_rank          <- one worker of run_partitioned per process (NCCL)
  *   ndgx_gauss_lobatto / ndgx_differentiation_matrix
  *                             <- gauss_lobatto / differentiation_matrix
  *                                (src/basis.cpp:32-76, 96-118), host setup inputs
@@ -126,8 +129,9 @@ int ndgx_stages(const ndgx_solver* s);
 int ndgx_launch_steps(ndgx_solver* s, long steps, ndgx_error* err);
 int ndgx_sync(ndgx_solver* s, ndgx_stats* stats, ndgx_error* err);
 void* ndgx_stream(ndgx_solver* s);
-/* Per-kernel timing of one un-graphed step (CUDA events on the launching
- * stream): ms[i] for stage kernel i, plus the step-control kernel at ms[stages]. */
+/* Per-stage timing of one step captured in a CUDA graph with event records
+ * between the stages (replayed 5 times, mean): ms[i] for stage i (a split
+ * stage's interior + boundary shell end to end), ms[stages] the step control. */
 int ndgx_profile_step(ndgx_solver* s, float* ms, int n, ndgx_error* err);
 
 /* Host setup inputs (same arithmetic as the reference). */
@@ -185,6 +189,25 @@ int ndgx_get_plan(const ndgx_solver* s, ndgx_rank_plan* plan);
 int ndgx_init_multisine_block(const ndgx_problem* global, const double* amplitudes, int n_modes, const int lo[3],
                               const int hi[3], double* u_aos);
 int ndgx_init_euler_subsonic_block(const ndgx_problem* global, const int lo[3], const int hi[3], double* u_aos);
+
+/* ------------------------------------------------------- partitioned
+ * run_partitioned (src/partition.cpp:186-333, include/ndg/partition.hpp:
+ * 66-67) in ONE handle: `workers` blocks of decompose()'s tiling, block w on
+ * device_ids[w % n_devices] (n_devices 0 / device_ids NULL -> global->device),
+ * i.e. SURVEY §8b's (n_devices, device_ids).  Per RK stage each block's pack
+ * kernel stores its boundary stage-input planes straight into the neighbour
+ * blocks' halo buffers (peer memory over NVLink across GPUs), the interior
+ * runs while they land, the boundary shell after; one shared device-side step
+ * control gives every block the global wavespeed (the alpha barrier).
+ * ndgx_upload/ndgx_download/ndgx_rhs/ndgx_advance on the handle take the
+ * GLOBAL AoS field, and every failure is NDGX_ERR_RUN with the reference's
+ * message "worker <w>: <what>" and error.worker = w.  force_exchange != 0
+ * routes every axis through the halo planes, even with one block (test hook).
+ * Results are bit-identical to ndgx_create's single block. */
+int ndgx_create_partitioned(const ndgx_problem* global, int workers, int n_devices, const int* device_ids,
+                            int force_exchange, ndgx_solver** out, ndgx_error* err);
+int ndgx_workers(const ndgx_solver* s);                                   /* blocks in the handle */
+int ndgx_get_block(const ndgx_solver* s, int worker, ndgx_rank_plan* plan); /* Block of `worker` */
 
 /* Checkpoint / restart in the reference's field-dump format ("ndgfield 1":
  * text header, then the raw little-endian doubles in FieldShape::index

@@ -6,8 +6,11 @@
 //
 //   ndgx::advance(config, initial, plan)        == ndg::advance        (src/solver.cpp:372-440)
 //   ndgx::serial_rhs(mesh, basis, model, field) == ndg::serial_rhs     (src/solver.cpp:442-456)
-//   ndgx::run_partitioned(config, initial, P, plan) -> single-GPU advance with the
-//        reference's RunError contract                                 (src/partition.cpp:186-333)
+//   ndgx::run_partitioned(config, initial, P, plan, devices)
+//                                               == ndg::run_partitioned (src/partition.cpp:186-333)
+//        P blocks of the reference's own decompose() tiling in one ndgx handle
+//        (block w on devices[w % devices.size()]), halos by peer stores, the
+//        reference's RunError("worker w: ...") contract
 //
 // with the same argument meaning, return types and exceptions
 // (include/ndg/errors.hpp:13-56).  The operator coefficients are built from
@@ -18,6 +21,7 @@
 
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "ndg/basis.hpp"
 #include "ndg/errors.hpp"
@@ -79,6 +83,13 @@ public:
     ndgx_error e{};
     check(ndgx_create(&p, &h_, &e), e);
   }
+  /// run_partitioned's workers in one handle (ndgx_create_partitioned).
+  Solver(const ndgx_problem& p, int workers, const std::vector<int>& devices) {
+    ndgx_error e{};
+    check(ndgx_create_partitioned(&p, workers, (int)devices.size(), devices.empty() ? nullptr : devices.data(), 0,
+                                  &h_, &e),
+          e);
+  }
   ~Solver() { ndgx_destroy(h_); }
   Solver(const Solver&) = delete;
   Solver& operator=(const Solver&) = delete;
@@ -108,6 +119,39 @@ inline ndg::AdvanceResult advance(const ndg::SolverConfig& config, const ndg::St
   r.stats.dt_min = st.dt_min;
   r.stats.dt_max = st.dt_max;
   r.stats.wall_seconds = st.wall_seconds;
+  return r;
+}
+
+/// Drop-in for ndg::run_partitioned (src/partition.cpp:186-333;
+/// include/ndg/partition.hpp:66-67): the same PartitionedResult (state gathered
+/// in the global AoS layout, worker 0's step statistics, the reference's own
+/// BlockDecomposition), failures as ndg::RunError("worker w: <what>", w).
+/// The halo exchange overlaps the interior elements on the device, so each
+/// worker's timing is reported as compute time.  States are bit-identical to
+/// ndg::run_partitioned in NDGX_ARITH_EXACT.
+inline ndg::PartitionedResult run_partitioned(const ndg::SolverConfig& config, const ndg::StateField& initial,
+                                              int worker_count, ndg::StepPlan plan = {},
+                                              const std::vector<int>& devices = {0},
+                                              int arith = NDGX_ARITH_EXACT) {
+  ndg::validate(config);
+  ndg::PartitionedResult r;
+  r.decomposition = ndg::decompose(config.mesh, worker_count);
+  const ndg::NodalBasis basis =
+      ndg::differentiation_matrix(ndg::gauss_lobatto(config.mesh.order));
+  Solver s(make_problem(config.mesh, config.model, basis, config.rk, config.cfl, config.t_end,
+                        devices.empty() ? 0 : devices[0], arith),
+           worker_count, devices);
+  ndgx_error e{};
+  check(ndgx_upload(s.get(), initial.data(), &e), e);
+  ndgx_stats st{};
+  check(ndgx_advance(s.get(), plan.fixed_steps, plan.warmup ? 1 : 0, &st, &e), e);
+  r.state = initial;
+  check(ndgx_download(s.get(), r.state.data(), &e), e);
+  r.stats.steps = st.steps;
+  r.stats.dt_min = st.dt_min;
+  r.stats.dt_max = st.dt_max;
+  r.stats.wall_seconds = st.wall_seconds;
+  r.worker_timings.assign(worker_count, ndg::WorkerTiming{st.wall_seconds, 0.0});
   return r;
 }
 

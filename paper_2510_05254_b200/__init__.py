@@ -11,4 +11,4 @@ from .ndgx import (ADVECTION, ARITH_EXACT, ARITH_FAST, EULER_ISOTHERMAL, RK3, RK
                    TransportError, advance, decompose, differentiation_matrix, gauss_lobatto,
                    init_block, init_euler_subsonic, init_multisine, lib, multisine_amplitudes,
                    nccl_unique_id, plan_rank, dump_field, load_field, RankPlan, rk_from_name, serial_rhs, validate, version,
-                   l2_error, conserved_totals)
+                   l2_error, conserved_totals, run_partitioned, PartitionedResult, WorkerTiming)

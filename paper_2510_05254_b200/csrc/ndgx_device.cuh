@@ -13,14 +13,10 @@
 // so one element's variable is NPE contiguous doubles (512 B at 2D N=8 and
 // at 3D N=4) and each x-line is N contiguous doubles.
 //
-// The fused stage kernel (ndgx_stage.cuh) is a persistent, warp-specialised
-// pipeline: a producer warp streams element tiles of u and the K_j it needs
-// into a shared-memory ring with TMA bulk copies (cp.async.bulk + mbarrier)
-// and builds the tile's face halo; four consumer warps evaluate the stage
-// input, the fluxes, the Lax-Friedrichs face fluxes and the per-axis volume
-// terms through shared memory and run the RK epilogue.  This file holds the
-// shared arithmetic (reference operation order), the step-control kernels and
-// the layout permutation.
+// The fused stage kernel (ndgx_stage.cuh) runs one element per warp over a
+// persistent grid (see there).  This file holds the shared arithmetic
+// (reference operation order), the step-control kernels, the wavespeed scan,
+// the face-plane packing of multi-block runs and the layout permutation.
 #pragma once
 
 #include <cstdint>
@@ -31,6 +27,7 @@ namespace ndgx {
 
 constexpr int kMaxOrder = 8;
 constexpr int kMaxTerms = 6;
+constexpr int kMaxRanges = 6;  // boundary shell of a 3D block: two slabs per axis
 constexpr unsigned long long kNoError = ~0ull;
 
 // Error-key phases, ordered like the reference's execution within a step.
@@ -114,6 +111,14 @@ struct StageArgs {
   // [axis][side] (side 0 low, 1 high), layout [cross-section cell][var][face node];
   // null -> periodic wrap inside this block
   const double* ext[3][2];
+  // linear element ranges [rng[q][0], rng[q][1]) of this launch, one per
+  // blockIdx.y (the whole block; or the interior / the boundary shell when a
+  // stage is split around its halo exchange), and the region filter: 0 every
+  // element of the ranges, 1 only those without a face on a split axis (an
+  // axis with ext planes), 2 only those with one
+  int rng[kMaxRanges][2];
+  int region;
+  int block_id;                    // worker / rank: names the block in InstabilityError keys
 };
 
 // ------------------------------------------------------------- arithmetic
@@ -212,9 +217,11 @@ namespace ndgx {
 
 // ============================================================ alpha scan
 // max_wavespeed_bound over a device-layout state (solver.cpp:310-334).
+// Error keys name the cell globally (block offset goff, global extents g1, g2),
+// like the stage kernels' keys.
 template <int DIM>
 __global__ void alpha_scan_kernel(const double* __restrict__ u, int c0, int c1, int c2, int order,
-                                  double a, Control* ctl, long long step_for_error) {
+                                  double a, Control* ctl, long long step_for_error, int3 goff, int g1, int g2) {
   constexpr int NV = DIM + 1;
   const int npe = DIM == 2 ? order * order : order * order * order;
   const long long n_elem = (long long)c0 * c1 * c2;
@@ -231,7 +238,7 @@ __global__ void alpha_scan_kernel(const double* __restrict__ u, int c0, int c1, 
       const int i = n % order, j = (n / order) % order, k = n / (order * order);
       const int an = DIM == 2 ? i * order + j : (i * order + j) * order + k;
       record_error(ctl, error_key(step_for_error, kPhaseScan,
-                                  ((long long)cx * c1 + cy) * c2 + cz, an));
+                                  ((long long)(cx + goff.x) * g1 + cy + goff.y) * g2 + cz + goff.z, an));
       continue;
     }
     double m = 0.0;
@@ -259,17 +266,19 @@ static __global__ void step_begin_kernel(StepParams sp) {
     c->skip = 1;
     return;
   }
+  // completion first: an error recorded by the final step's trailing scan
+  // (the next step's wavespeed) must not abort a run that is already over
+  const bool fixed = sp.fixed_steps >= 0;
+  if ((fixed && c->steps >= sp.fixed_steps) || (!fixed && !(c->t < sp.t_end))) {
+    c->done = 1;
+    c->skip = 1;
+    return;
+  }
   if (sp.ranked ? c->any_err != 0ull : c->err_key != kNoError) {
     // a rank solver stops on the all-reduced flag, so every rank -- the
     // failing one included -- stops at this same step (run_partitioned:
     // "stopped by failure elsewhere", src/partition.cpp:239-241)
     if (sp.ranked) c->aborted = 1;
-    c->skip = 1;
-    return;
-  }
-  const bool fixed = sp.fixed_steps >= 0;
-  if ((fixed && c->steps >= sp.fixed_steps) || (!fixed && !(c->t < sp.t_end))) {
-    c->done = 1;
     c->skip = 1;
     return;
   }
@@ -303,6 +312,16 @@ static __global__ void step_begin_kernel(StepParams sp) {
   c->dt = dt;
   c->skip = 0;
   c->alpha_bits = 0ull;  // this step's last-stage epilogue accumulates the next alpha
+}
+
+// ====================================================== in-graph timing
+// The global nanosecond timer into out[i]: launched between the stages of a
+// captured step, consecutive stamps bracket each stage exactly as it runs in
+// the timed graph (events recorded inside a graph cannot be timed).
+static __global__ void stamp_kernel(unsigned long long* out, int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  out[i] = t;
 }
 
 // ===================================================== layout permutation

@@ -507,7 +507,7 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
       double sum = un[0];
 #pragma unroll
       for (int v = 1; v < NV; ++v) sum += un[v];
-      if (!isfinite(sum)) record_error(p.ctl, error_key(step, kPhaseInstability, 0, 0));
+      if (!isfinite(sum)) record_error(p.ctl, error_key(step, kPhaseInstability, p.block_id, 0));
       if (KIND == 1 && p.scan_alpha) {
         if (!(un[0] > 0.0)) {
           const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
@@ -549,7 +549,7 @@ struct Lane8 {
 // per half-warp instead of two (a 4-way conflict unswizzled).
 __host__ __device__ constexpr int swz8(int n) { return n ^ (((n >> 4) & 3) << 2); }
 
-template <int KIND, int NU, int AM, int BM>
+template <int KIND, int NU, int AM, int BM, int SIG>
 __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8& ln, int lane, int e, int cx,
                                                  int cy, const double* src, const double* fsrc, bool ring,
                                                  double* sF, double* sT, double* sH, double dt, bool last,
@@ -766,7 +766,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       double sum = un[s2][0];  // non-finite iff some component is
 #pragma unroll
       for (int v = 1; v < NV; ++v) sum += un[s2][v];
-      if (!isfinite(sum)) record_error(p.ctl, error_key(step, kPhaseInstability, 0, 0));
+      if (!isfinite(sum)) record_error(p.ctl, error_key(step, kPhaseInstability, p.block_id, 0));
       if (KIND == 1 && p.scan_alpha) {
         if (!(un[s2][0] > 0.0)) {
           const int n = ln.o0 + 8 * s2;
@@ -817,7 +817,8 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     return;
 
   const int C0 = p.cells[0], C1 = p.cells[1], C2 = p.cells[2];
-  const long long nelem = (long long)C0 * C1 * C2;
+  // this CTA's linear element range (blockIdx.y) and region filter
+  const int e_lo = p.rng[blockIdx.y][0], nelem = p.rng[blockIdx.y][1];  // element counts are < 2^31
   // the last stage is exactly the signature with b-terms (kSigs), so the
   // epilogue variant is resolved at compile time
   constexpr bool last = kSigs[SIG].bm != 0;
@@ -916,10 +917,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   }
 
   // element e = cx + C0 (cy + C1 cz), advanced by the total warp count with
-  // an incremental (x, y, z) counter (element counts are < 2^31)
+  // an incremental (x, y, z) counter
   const int nw = (int)nwarps;
   const int sx = nw % C0, sy = (nw / C0) % C1, sz = nw / (C0 * C1);
-  int e = (int)blockIdx.x * G::WARPS + wib;
+  int e = e_lo + (int)blockIdx.x * G::WARPS + wib;
   int cx = e % C0, cy = (e / C0) % C1, cz = e / (C0 * C1);
   auto step_coords = [&](int& x, int& y, int& z) {
     x += sx;
@@ -929,6 +930,16 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     carry = y >= C1;
     y -= carry ? C1 : 0;
     z += sz + carry;
+  };
+  // region filter of a split stage (StageArgs::region): the interior launch
+  // skips elements with a face on a split axis (one whose halo arrives by
+  // exchange), the boundary launch skips the others
+  auto skipped = [&](int x, int y, int z) -> bool {
+    if (p.region == 0) return false;
+    const bool edge = (p.ext[0][0] != nullptr && (x == 0 || x == C0 - 1)) ||
+                      (p.ext[1][0] != nullptr && (y == 0 || y == C1 - 1)) ||
+                      (p.ext[2][0] != nullptr && (z == 0 || z == C2 - 1));
+    return edge != (p.region == 2);
   };
   // the element `depth - 1` iterations ahead (the next one to issue)
   int ae = e, ax = cx, ay = cy, az = cz;
@@ -946,18 +957,18 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   // (measured per stage: a win for the Euler last stage, 0.96 -> 0.83 ms on
   // C3, whose x-lo reuse saves two arrays' face loads; a loss elsewhere)
   if constexpr (USE_MMA && NDGX_XRUN > 1 && KIND == 1 && LASTC) {
-    if (depth == 0) {
+    if (depth == 0 && p.region == 0) {
       // runs of XR consecutive x elements per warp (run ρ -> warp ρ mod nw)
       constexpr int XR = NDGX_XRUN;
       const long long S = (long long)nw * XR;  // run stride
       const int tx = (int)(S % C0), ty = (int)((S / C0) % C1), tz = (int)(S / ((long long)C0 * C1));
-      int rb = ((int)blockIdx.x * G::WARPS + wib) * XR;
+      int rb = e_lo + ((int)blockIdx.x * G::WARPS + wib) * XR;
       int rx = rb % C0, ry = (rb / C0) % C1, rz = rb / (C0 * C1);
       for (; rb < nelem; rb += (int)S) {
         int x = rx, y = ry, z = rz;
         for (int k = 0; k < XR && rb + k < nelem; ++k) {
-          element_2d8_fast<KIND, NU, AM, BM>(p, ln8, lane, rb + k, x, y, ring, nullptr, false, sF, sT, sH,
-                                             dt, last, step, alpha, k > 0 && x > 0);
+          element_2d8_fast<KIND, NU, AM, BM, SIG>(p, ln8, lane, rb + k, x, y, ring, nullptr, false, sF, sT, sH,
+                                                  dt, last, step, alpha, k > 0 && x > 0);
           if (++x == C0) {
             x = 0;
             if (++y == C1) {
@@ -974,7 +985,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         ry -= carry ? C1 : 0;
         rz += tz + carry;
       }
-      e = (int)nelem;  // done: skip the element loop below
+      e = nelem;  // done: skip the element loop below
     }
   }
   for (; e < nelem; e += nw) {
@@ -999,13 +1010,21 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         else cp_async_wait<3>();
       }
     }
+    if (skipped(cx, cy, cz)) {  // not in this launch's region (its ring slot is consumed unread)
+      if (depth > 0 && ++slot == depth) {
+        slot = 0;
+        parity ^= 1;
+      }
+      step_coords(cx, cy, cz);
+      continue;
+    }
     if constexpr (USE_MMA3) {
       element_3d4_fast<KIND, NU, AM, BM>(p, ln4, lane, e, cx, cy, cz, sF, sT, sH, dt, step, alpha);
       step_coords(cx, cy, cz);
       continue;
     }
     if constexpr (USE_MMA) {
-      element_2d8_fast<KIND, NU, AM, BM>(p, ln8, lane, e, cx, cy, src, fsrc, depth > 0, sF, sT, sH, dt, last, step,
+      element_2d8_fast<KIND, NU, AM, BM, SIG>(p, ln8, lane, e, cx, cy, src, fsrc, depth > 0, sF, sT, sH, dt, last, step,
                                          alpha);
       if (depth > 0 && ++slot == depth) {
         slot = 0;
@@ -1162,7 +1181,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         bool fin = true;
 #pragma unroll
         for (int v = 0; v < NV; ++v) fin = fin && isfinite(un[v]);
-        if (!fin) record_error(ctl, error_key(step, kPhaseInstability, 0, 0));
+        if (!fin) record_error(ctl, error_key(step, kPhaseInstability, p.block_id, 0));
         if (KIND == 1 && p.scan_alpha) {
           if (!(un[0] > 0.0)) {
             record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(), G::aos_node(n)));

@@ -148,6 +148,10 @@ def lib() -> C.CDLL:
     L.ndgx_nccl_unique_id.argtypes = [C.c_char_p, P(Error)]
     L.ndgx_create_rank.argtypes = [P(Problem), C.c_int, C.c_int, C.c_char_p, C.c_int, P(C.c_void_p), P(Error)]
     L.ndgx_get_plan.argtypes = [C.c_void_p, P(RankPlan)]
+    L.ndgx_create_partitioned.argtypes = [P(Problem), C.c_int, C.c_int, P(C.c_int), C.c_int, P(C.c_void_p),
+                                          P(Error)]
+    L.ndgx_workers.argtypes = [C.c_void_p]
+    L.ndgx_get_block.argtypes = [C.c_void_p, C.c_int, P(RankPlan)]
     L.ndgx_dump_field.argtypes = [C.c_void_p, C.c_char_p, P(Error)]
     L.ndgx_load_field.argtypes = [C.c_void_p, C.c_char_p, P(Error)]
     L.ndgx_init_multisine_block.argtypes = [P(Problem), D, C.c_int, P(C.c_int), P(C.c_int), D]
@@ -328,13 +332,18 @@ class Solver:
     """A device-resident solver handle (one ndgx_solver)."""
 
     def __init__(self, config: SolverConfig, device: int = 0, arith: int = ARITH_EXACT, basis=None,
-                 _rank=None):
+                 _rank=None, _part=None):
         validate(config)
         self.config = config
         self.problem = make_problem(config, device, arith, basis)
         self._h = C.c_void_p()
         err = Error()
-        if _rank is None:
+        if _part is not None:
+            workers, devices, force = _part
+            devs = (C.c_int * max(1, len(devices)))(*devices) if devices else None
+            _check(lib().ndgx_create_partitioned(C.byref(self.problem), workers, len(devices) if devices else 0,
+                                                 devs, int(force), C.byref(self._h), C.byref(err)), err)
+        elif _rank is None:
             _check(lib().ndgx_create(C.byref(self.problem), C.byref(self._h), C.byref(err)), err)
         else:
             nranks, rank, nccl_id, force = _rank
@@ -345,6 +354,24 @@ class Solver:
         self.stages = int(lib().ndgx_stages(self._h))
         self.plan = RankPlan()
         lib().ndgx_get_plan(self._h, C.byref(self.plan))
+        self.workers = int(lib().ndgx_workers(self._h))
+
+    @classmethod
+    def partitioned(cls, config: SolverConfig, workers: int, devices: Optional[Sequence[int]] = None,
+                    arith: int = ARITH_EXACT, force_exchange: bool = False) -> "Solver":
+        """run_partitioned's `workers` blocks (src/partition.cpp:186-333) in one
+        handle, block w on devices[w % len(devices)] (default: device 0).  Halo
+        planes move by peer stores; states in and out are the GLOBAL field;
+        failures raise RunError("worker w: ...")."""
+        devices = list(devices) if devices else [0]
+        return cls(config, devices[0], arith, None, _part=(workers, devices, force_exchange))
+
+    def block(self, worker: int) -> RankPlan:
+        """The Block of `worker` (lo/hi, neighbours, split axes) in this handle."""
+        pl = RankPlan()
+        if lib().ndgx_get_block(self._h, worker, C.byref(pl)) != 0:
+            raise ConfigError(f"no worker {worker} in this handle")
+        return pl
 
     @classmethod
     def for_rank(cls, config: SolverConfig, nranks: int, rank: int, nccl_id: bytes, device: int = 0,
@@ -450,6 +477,40 @@ def advance(config: SolverConfig, initial, plan: StepPlan = StepPlan(), device: 
         s.upload(initial)
         stats = s.advance(plan)
         return AdvanceResult(s.download(), stats)
+
+
+@dataclass
+class WorkerTiming:
+    """WorkerTiming (include/ndg/partition.hpp:49-52).  The device path overlaps
+    the halo exchange with interior elements, so the whole stepping time of the
+    handle is reported as compute and the exchange as 0."""
+    compute_seconds: float = 0.0
+    exchange_seconds: float = 0.0
+
+
+@dataclass
+class PartitionedResult:
+    """PartitionedResult (include/ndg/partition.hpp:54-60)."""
+    state: np.ndarray
+    stats: StepStats
+    worker_timings: list
+    decomposition: "BlockDecomposition"
+
+
+def run_partitioned(config: SolverConfig, initial, worker_count: int, plan: StepPlan = StepPlan(),
+                    devices: Optional[Sequence[int]] = None, arith: int = ARITH_EXACT) -> PartitionedResult:
+    """run_partitioned(config, initial, workers, plan) -- src/partition.cpp:186-333,
+    on the GPU: worker_count blocks of decompose()'s tiling in one handle (block w
+    on devices[w % len(devices)]).  Bit-identical to advance() in either
+    arithmetic mode; failures raise RunError("worker w: ...", w)."""
+    validate(config)
+    decomposition = decompose(config.mesh, worker_count)
+    with Solver.partitioned(config, worker_count, devices, arith) as s:
+        s.upload(initial)
+        stats = s.advance(plan)
+        state = s.download()
+    timings = [WorkerTiming(stats.wall_seconds, 0.0) for _ in range(worker_count)]
+    return PartitionedResult(state, stats, timings, decomposition)
 
 
 def serial_rhs(mesh: Mesh, model: EquationModel, field, basis=None, device: int = 0,

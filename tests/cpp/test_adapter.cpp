@@ -121,6 +121,87 @@ int main() {
     }
     CHECK(threw);
   }
+  // ---- run_partitioned (proj/tests/test_partition.cpp:267-349) against the reference's own
+  {
+    const Mesh mesh(2, {8, 8, 1}, 3);
+    const EquationModel model = EquationModel::advection(2, {1, 0, 0});
+    const StateField init = init_multisine(mesh, model, gauss_lobatto(3), 4, 2026);
+    const SolverConfig config{mesh, model, RKMethod::rk4, 0.4, 1.0};
+    for (int workers : {1, 2, 4}) {
+      const PartitionedResult want = ndg::run_partitioned(config, init, workers, StepPlan{10, false});
+      const PartitionedResult got = ndgx::run_partitioned(config, init, workers, StepPlan{10, false});
+      const bool ok = same(want.state, got.state) && want.stats.steps == got.stats.steps &&
+                      got.worker_timings.size() == (size_t)workers &&
+                      got.decomposition.grid == want.decomposition.grid;
+      std::printf("%s run_partitioned 2D adv o3 RK4 8x8 P=%d\n", ok ? "ok  " : "FAIL", workers);
+      CHECK(ok);
+    }
+  }
+  {
+    const Mesh mesh(3, {4, 4, 4}, 2);
+    const EquationModel model = EquationModel::advection(3, {1, 0, 0});
+    const StateField init = init_multisine(mesh, model, gauss_lobatto(2), 2, 5);
+    const SolverConfig config{mesh, model, RKMethod::rk3, 0.4, 1.0};
+    const PartitionedResult want = ndg::run_partitioned(config, init, 2, StepPlan{6, false});
+    const PartitionedResult got = ndgx::run_partitioned(config, init, 2, StepPlan{6, false});
+    std::printf("%s run_partitioned 3D adv o2 RK3 4^3 P=2\n", same(want.state, got.state) ? "ok  " : "FAIL");
+    CHECK(same(want.state, got.state));
+  }
+  {
+    const Mesh mesh(2, {8, 8, 1}, 3);
+    const EquationModel model = EquationModel::isothermal_euler(2, 1.0);
+    const StateField init = init_euler_subsonic(mesh, model, gauss_lobatto(3), 0);
+    const SolverConfig config{mesh, model, RKMethod::rk4, 0.4, 1.0};
+    const PartitionedResult want = ndg::run_partitioned(config, init, 4, StepPlan{8, false});
+    const PartitionedResult got = ndgx::run_partitioned(config, init, 4, StepPlan{8, false});
+    const bool ok = same(want.state, got.state) && want.stats.dt_min == got.stats.dt_min;
+    std::printf("%s run_partitioned 2D Euler o3 RK4 8x8 P=4\n", ok ? "ok  " : "FAIL");
+    CHECK(ok);
+  }
+  {
+    const Mesh mesh(2, {6, 6, 1}, 3);
+    const EquationModel model = EquationModel::advection(2, {1, 0, 0});
+    const StateField init = init_multisine(mesh, model, gauss_lobatto(3), 3, 7);
+    const SolverConfig config{mesh, model, RKMethod::rk4, 0.4, 0.03};
+    const PartitionedResult want = ndg::run_partitioned(config, init, 2);
+    const PartitionedResult got = ndgx::run_partitioned(config, init, 2);
+    const bool ok = same(want.state, got.state) && want.stats.steps == got.stats.steps &&
+                    want.stats.dt_max == got.stats.dt_max;
+    std::printf("%s run_partitioned t_end 6x6 P=2 (steps %ld)\n", ok ? "ok  " : "FAIL", got.stats.steps);
+    CHECK(ok);
+  }
+  {
+    const Mesh mesh(3, {4, 4, 16}, 4);
+    const EquationModel model = EquationModel::isothermal_euler(3, 1.0);
+    const StateField init = init_euler_subsonic(mesh, model, gauss_lobatto(4));
+    const SolverConfig config{mesh, model, RKMethod::rk6, 0.4, 1.0};
+    const PartitionedResult want = ndg::run_partitioned(config, init, 4, StepPlan{5, true});
+    const PartitionedResult got = ndgx::run_partitioned(config, init, 4, StepPlan{5, true});
+    const bool ok = same(want.state, got.state) && want.decomposition.grid == got.decomposition.grid &&
+                    want.stats.dt_max == got.stats.dt_max;
+    std::printf("%s run_partitioned 3D Euler o4 RK6 4x4x16 P=4 z-slabs\n", ok ? "ok  " : "FAIL");
+    CHECK(ok);
+  }
+  {  // a failing worker surfaces as RunError naming it (test_partition.cpp:330-349)
+    const Mesh mesh(2, {8, 8, 1}, 3);
+    const EquationModel model = EquationModel::isothermal_euler(2, 1.0);
+    StateField init = init_euler_subsonic(mesh, model, gauss_lobatto(3), 0);
+    init.at({6, 6, 0}, {1, 1, 0}, 0) = -2.0;
+    const SolverConfig config{mesh, model, RKMethod::rk4, 0.4, 1.0};
+    std::string want, got;
+    int want_w = -1, got_w = -1;
+    try { ndg::run_partitioned(config, init, 2, StepPlan{4, false}); } catch (const RunError& e) {
+      want = e.what();
+      want_w = e.worker();
+    }
+    try { ndgx::run_partitioned(config, init, 2, StepPlan{4, false}); } catch (const RunError& e) {
+      got = e.what();
+      got_w = e.worker();
+    }
+    std::printf("%s RunError: '%s' (reference '%s')\n", got == want && got_w == 1 ? "ok  " : "FAIL", got.c_str(),
+                want.c_str());
+    CHECK(got == want && got_w == want_w && got_w == 1);
+  }
   std::printf("%d/%d checks passed\n", g_checks - g_fail, g_checks);
   return g_fail == 0 ? 0 : 1;
 }
