@@ -111,13 +111,16 @@ struct StageArgs {
   // [axis][side] (side 0 low, 1 high), layout [cross-section cell][var][face node];
   // null -> periodic wrap inside this block
   const double* ext[3][2];
-  // linear element ranges [rng[q][0], rng[q][1]) of this launch, one per
-  // blockIdx.y (the whole block; or the interior / the boundary shell when a
-  // stage is split around its halo exchange), and the region filter: 0 every
-  // element of the ranges, 1 only those without a face on a split axis (an
-  // axis with ext planes), 2 only those with one
-  int rng[kMaxRanges][2];
+  // element ranges of this launch, one per blockIdx.y: e = rng[q][0],
+  // rng[q][0] + rng[q][2], ... < rng[q][1] (the whole block; or the interior
+  // / the boundary shell when a stage is split around its halo exchange:
+  // contiguous runs, whole x-columns at stride C0), and the region filter:
+  // 0 every element of the ranges, 1 only those inside the box
+  // [inner[0], inner[1]), 2 only those outside it, 3 like 1 where the
+  // range's rows all lie inside the box in y and z (only x is tested)
+  int rng[kMaxRanges][3];
   int region;
+  int inner[2][3];
   int block_id;                    // worker / rank: names the block in InstabilityError keys
 };
 

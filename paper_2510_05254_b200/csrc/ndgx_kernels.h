@@ -11,6 +11,7 @@ using StageFn = void (*)(const StageArgs);
 
 struct StageKernel {
   StageFn fn[kNumSigs] = {};  // by stage signature (kSigs)
+  StageFn fnx[kNumSigs] = {}; // region-3 (x-filtered interior) launches: the x-run variant where one exists
   int threads = 0;
   int warps = 0;            // elements in flight per CTA (one per warp)
   int smem_fixed[kNumSigs] = {};  // dynamic shared memory without the element rings, per signature
@@ -41,6 +42,15 @@ StageKernel make_stage_kernel() {
   k.fn[6] = &stage_kernel<DIM, N, KIND, EXACT, 6>;
   k.fn[7] = &stage_kernel<DIM, N, KIND, EXACT, 7>;
   k.fn[8] = &stage_kernel<DIM, N, KIND, EXACT, 8>;
+  // the x-run body (2D order-8 contracted Euler, last stages) has an
+  // x-filtered twin; every other kernel handles region 3 in its element loop
+  constexpr bool XRUN = G::MMA && !EXACT && KIND == 1;
+  for (int q = 0; q < kNumSigs; ++q) k.fnx[q] = k.fn[q];
+  if constexpr (XRUN) {
+    k.fnx[2] = &stage_kernel<DIM, N, KIND, EXACT, 2, true>;
+    k.fnx[3] = &stage_kernel<DIM, N, KIND, EXACT, 3, true>;
+    k.fnx[8] = &stage_kernel<DIM, N, KIND, EXACT, 8, true>;
+  }
   k.threads = G::THREADS;
   k.warps = G::WARPS;
   for (int q = 0; q < kNumSigs; ++q)

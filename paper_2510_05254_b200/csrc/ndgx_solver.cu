@@ -98,8 +98,9 @@ struct Box {
 // each) and the region filter (StageArgs::rng / region).
 struct Launch {
   int n = 0;
-  int rng[ndgx::kMaxRanges][2] = {};
+  int rng[ndgx::kMaxRanges][3] = {};  // begin, end, stride
   int region = 0;
+  int inner[2][3] = {};
 };
 
 enum Mode { kNoExchange = 0, kNccl = 1, kDirect = 2 };
@@ -125,42 +126,60 @@ struct Blk {
   Launch whole, inner, shell;       // the whole block; interior / boundary shell of a split stage
 
   long long lin(int x, int y, int z) const { return x + (long long)cells[0] * (y + (long long)cells[1] * z); }
-  // the elements of box b are one contiguous run of the block's element order
-  bool contiguous(const Box& b) const {
+  // the elements of box b as one range (begin, end, stride): a contiguous run
+  // of the block's element order, or a run of whole x-columns at stride C0
+  bool as_range(const Box& b, int r[3]) const {
     int h = 0;
     for (int a = 0; a < 3; ++a)
       if (b.n[a] > 1) h = a;
-    for (int a = 0; a < h; ++a)
-      if (b.n[a] != cells[a]) return false;
-    return true;
+    bool run = true;
+    for (int a = 0; a < h; ++a) run = run && b.n[a] == cells[a];
+    const long long f = lin(b.o[0], b.o[1], b.o[2]);
+    const long long l = lin(b.o[0] + b.n[0] - 1, b.o[1] + b.n[1] - 1, b.o[2] + b.n[2] - 1);
+    if (run) {
+      r[0] = (int)f;
+      r[1] = (int)l + 1;
+      r[2] = 1;
+      return true;
+    }
+    // one x, a contiguous run of (y, z)
+    if (b.n[0] == 1 && (b.n[2] == 1 || b.n[1] == cells[1])) {
+      r[0] = (int)f;
+      r[1] = (int)l + 1;
+      r[2] = cells[0];
+      return true;
+    }
+    return false;
   }
-  void first_last(const Box& b, long long& f, long long& l) const {
-    f = lin(b.o[0], b.o[1], b.o[2]);
-    l = lin(b.o[0] + b.n[0] - 1, b.o[1] + b.n[1] - 1, b.o[2] + b.n[2] - 1) + 1;
-  }
-  // Launches for a set of boxes: one range each when every box is a
-  // contiguous run, else one range spanning them all with the region filter
-  // (whose skipped elements are exactly the span's elements outside the set).
-  Launch launch_of(const std::vector<Box>& boxes, int region) const {
+  // Launch over a set of boxes: one range each when they all are ranges,
+  // else one contiguous span of them all with the region filter against the
+  // interior box `in` (the span's elements outside the set are exactly those
+  // the filter skips).
+  Launch launch_of(const std::vector<Box>& boxes, int region, const Box& in) const {
     Launch L;
-    bool runs = boxes.size() <= (size_t)ndgx::kMaxRanges;
-    for (const Box& b : boxes) runs = runs && contiguous(b);
+    for (int a = 0; a < 3; ++a) {
+      L.inner[0][a] = in.o[a];
+      L.inner[1][a] = in.o[a] + in.n[a];
+    }
+    bool ranges = boxes.size() <= (size_t)ndgx::kMaxRanges;
     long long lo = -1, hi = -1;
     for (const Box& b : boxes) {
-      long long f, l;
-      first_last(b, f, l);
-      if (runs) {
-        L.rng[L.n][0] = (int)f;
-        L.rng[L.n][1] = (int)l;
+      int r[3];
+      ranges = ranges && as_range(b, r);
+      if (ranges) {
+        for (int q = 0; q < 3; ++q) L.rng[L.n][q] = r[q];
         ++L.n;
       }
+      const long long f = lin(b.o[0], b.o[1], b.o[2]);
+      const long long l = lin(b.o[0] + b.n[0] - 1, b.o[1] + b.n[1] - 1, b.o[2] + b.n[2] - 1) + 1;
       lo = lo < 0 ? f : std::min(lo, f);
       hi = std::max(hi, l);
     }
-    if (!runs && !boxes.empty()) {
+    if (!ranges && !boxes.empty()) {
       L.n = 1;
       L.rng[0][0] = (int)lo;
       L.rng[0][1] = (int)hi;
+      L.rng[0][2] = 1;
       L.region = region;
     }
     return L;
@@ -171,7 +190,7 @@ struct Blk {
   void make_launches() {
     Box all;
     for (int a = 0; a < 3; ++a) all.n[a] = cells[a];
-    whole = launch_of({all}, 0);
+    whole = launch_of({all}, 0, all);
     Box rest = all;
     std::vector<Box> sh;
     for (int a = 0; a < 3; ++a) {
@@ -185,8 +204,11 @@ struct Blk {
       rest.o[a] += 1;
       rest.n[a] = std::max(0, rest.n[a] - 2);
     }
-    inner = rest.count() > 0 ? launch_of({rest}, 1) : Launch{};
-    shell = launch_of(sh, 2);
+    inner = rest.count() > 0 ? launch_of({rest}, 1, rest) : Launch{};
+    // the span of the interior box holds only interior rows when its (y, z)
+    // part is one run: then only x needs testing (region 3)
+    if (inner.region == 1 && (rest.n[2] == 1 || rest.n[1] == cells[1])) inner.region = 3;
+    shell = launch_of(sh, 2, rest);
   }
 };
 
@@ -369,19 +391,21 @@ struct ndgx_solver {
     StageArgs s = s0;
     long long most = 0;
     for (int q = 0; q < L.n; ++q) {
-      s.rng[q][0] = L.rng[q][0];
-      s.rng[q][1] = L.rng[q][1];
-      most = std::max<long long>(most, L.rng[q][1] - L.rng[q][0]);
+      for (int x = 0; x < 3; ++x) s.rng[q][x] = L.rng[q][x];
+      most = std::max<long long>(most, (L.rng[q][1] - L.rng[q][0] + L.rng[q][2] - 1) / L.rng[q][2]);
     }
     s.region = L.region;
-    // a boundary shell spread over the block reads HBM directly: a ring would
-    // stream the elements it skips
-    if (L.region == 2) s.depth = 0;
+    std::memcpy(s.inner, L.inner, sizeof(s.inner));
+    // a boundary shell spread over the block, or whole x-columns, read HBM
+    // directly: a ring would stream the elements it skips / lose its locality
+    if (L.region == 2 || (L.n > 0 && L.rng[0][2] != 1)) s.depth = 0;
+    for (int q = 0; q < L.n; ++q)
+      if (L.rng[q][2] != 1) s.depth = 0;
     // persistent CTAs (one element per warp): as many as are co-resident
     const long long need = (most + kern.warps - 1) / kern.warps;
     const ndgx::StageLaunch& c = lcfg[s.sig];
     const long long grid = std::max<long long>(1, std::min<long long>(need, (long long)c.grid));
-    kern.fn[s.sig]<<<dim3((unsigned)grid, (unsigned)L.n), kern.threads, c.smem, st>>>(s);
+    (L.region == 3 ? kern.fnx : kern.fn)[s.sig]<<<dim3((unsigned)grid, (unsigned)L.n), kern.threads, c.smem, st>>>(s);
   }
 
   void fork() const {
@@ -606,6 +630,10 @@ struct ndgx_solver {
         return NDGX_ERR_CONFIG;
       }
       ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, best.smem), "smem attribute");
+      if (kern.fnx[q] != kern.fn[q])
+        ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern.fnx[q]),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, best.smem),
+           "smem attribute");
       lcfg[q] = best;
     }
     return NDGX_OK;

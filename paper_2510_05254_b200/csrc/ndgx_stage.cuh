@@ -788,7 +788,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
 // ============================================================ stage kernel
 // SIG indexes kSigs: the stage's term structure (p.nu, p.amask, p.bmask) at
 // compile time, so the term loops resolve without predicates
-template <int DIM, int N, int KIND, bool EXACT, int SIG>
+template <int DIM, int N, int KIND, bool EXACT, int SIG, bool XF = false>
 // <= 128 registers (4 CTAs = 16 warps per SM): capping at 80 for 24 warps
 // measured 25% slower (less load-level parallelism per warp)
 #ifndef NDGX_MINB
@@ -817,8 +817,9 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     return;
 
   const int C0 = p.cells[0], C1 = p.cells[1], C2 = p.cells[2];
-  // this CTA's linear element range (blockIdx.y) and region filter
+  // this CTA's element range (blockIdx.y): e = begin, begin + stride, ... < end
   const int e_lo = p.rng[blockIdx.y][0], nelem = p.rng[blockIdx.y][1];  // element counts are < 2^31
+  const int e_stride = p.rng[blockIdx.y][2];
   // the last stage is exactly the signature with b-terms (kSigs), so the
   // epilogue variant is resolved at compile time
   constexpr bool last = kSigs[SIG].bm != 0;
@@ -916,11 +917,12 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     }
   }
 
-  // element e = cx + C0 (cy + C1 cz), advanced by the total warp count with
-  // an incremental (x, y, z) counter
+  // element e = cx + C0 (cy + C1 cz), advanced by the total warp count times
+  // the range stride with an incremental (x, y, z) counter
   const int nw = (int)nwarps;
-  const int sx = nw % C0, sy = (nw / C0) % C1, sz = nw / (C0 * C1);
-  int e = e_lo + (int)blockIdx.x * G::WARPS + wib;
+  const int es = nw * e_stride;  // element step (< 2^31: ranges stay inside the block)
+  const int sx = es % C0, sy = (es / C0) % C1, sz = es / (C0 * C1);
+  int e = e_lo + ((int)blockIdx.x * G::WARPS + wib) * e_stride;
   int cx = e % C0, cy = (e / C0) % C1, cz = e / (C0 * C1);
   auto step_coords = [&](int& x, int& y, int& z) {
     x += sx;
@@ -932,21 +934,20 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     z += sz + carry;
   };
   // region filter of a split stage (StageArgs::region): the interior launch
-  // skips elements with a face on a split axis (one whose halo arrives by
-  // exchange), the boundary launch skips the others
+  // takes only the elements inside p.inner (no face on a split axis), the
+  // boundary launch only those outside it
   auto skipped = [&](int x, int y, int z) -> bool {
     if (p.region == 0) return false;
-    const bool edge = (p.ext[0][0] != nullptr && (x == 0 || x == C0 - 1)) ||
-                      (p.ext[1][0] != nullptr && (y == 0 || y == C1 - 1)) ||
-                      (p.ext[2][0] != nullptr && (z == 0 || z == C2 - 1));
-    return edge != (p.region == 2);
+    const bool in = x >= p.inner[0][0] && x < p.inner[1][0] && y >= p.inner[0][1] && y < p.inner[1][1] &&
+                    z >= p.inner[0][2] && z < p.inner[1][2];
+    return in == (p.region == 2);  // regions 1 and 3 take the inside
   };
   // the element `depth - 1` iterations ahead (the next one to issue)
   int ae = e, ax = cx, ay = cy, az = cz;
   for (int q = 0; q + 1 < depth; ++q) {
     if (ae < nelem) issue(ae, ax, ay, az, q);
     else if (G::FACE_PF) cp_async_commit();  // keep one group per slot
-    ae += nw;
+    ae += es;
     step_coords(ax, ay, az);
   }
   int slot = 0;
@@ -957,8 +958,12 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   // (measured per stage: a win for the Euler last stage, 0.96 -> 0.83 ms on
   // C3, whose x-lo reuse saves two arrays' face loads; a loss elsewhere)
   if constexpr (USE_MMA && NDGX_XRUN > 1 && KIND == 1 && LASTC) {
-    if (depth == 0 && p.region == 0) {
+    // (unfiltered contiguous launches, or x-filtered ones in the XF
+    // instantiation: a region test inside the runs perturbs this
+    // register-capped body, so the unfiltered kernel carries none)
+    if (depth == 0 && e_stride == 1 && p.region == (XF ? 3 : 0)) {
       // runs of XR consecutive x elements per warp (run ρ -> warp ρ mod nw)
+      const int X0 = XF ? p.inner[0][0] : 0, X1 = XF ? p.inner[1][0] : C0;
       constexpr int XR = NDGX_XRUN;
       const long long S = (long long)nw * XR;  // run stride
       const int tx = (int)(S % C0), ty = (int)((S / C0) % C1), tz = (int)(S / ((long long)C0 * C1));
@@ -967,8 +972,11 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       for (; rb < nelem; rb += (int)S) {
         int x = rx, y = ry, z = rz;
         for (int k = 0; k < XR && rb + k < nelem; ++k) {
-          element_2d8_fast<KIND, NU, AM, BM, SIG>(p, ln8, lane, rb + k, x, y, ring, nullptr, false, sF, sT, sH,
-                                                  dt, last, step, alpha, k > 0 && x > 0);
+          // region 3: the rows of the range are interior, only x in [X0, X1) is
+          // taken, and the x-lo neighbour is in the slab for x > X0
+          if (!XF || (x >= X0 && x < X1))
+            element_2d8_fast<KIND, NU, AM, BM, SIG>(p, ln8, lane, rb + k, x, y, ring, nullptr, false, sF, sT, sH,
+                                                    dt, last, step, alpha, k > 0 && x > X0);
           if (++x == C0) {
             x = 0;
             if (++y == C1) {
@@ -988,7 +996,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       e = nelem;  // done: skip the element loop below
     }
   }
-  for (; e < nelem; e += nw) {
+  for (; e < nelem; e += es) {
     const size_t ebase = (size_t)e * NV * NPE;
     const double* src = ring + slot * SLOT;  // this element's u and K_j (when depth > 0)
     const double* fsrc = src + (1 + NU) * G::CHUNK;  // its face neighbour values (FACE_PF)
@@ -1000,7 +1008,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       } else if (G::FACE_PF) {
         cp_async_commit();
       }
-      ae += nw;
+      ae += es;
       step_coords(ax, ay, az);
       mbar_wait(&bar[slot], parity);
       if constexpr (G::FACE_PF) {
