@@ -12,6 +12,11 @@ initial condition (synthetic), cfl 0.4, periodic unit box.
   4 fused stage kernels per step), CUDA events on the solver's stream, after
   W warm-up steps; max over ranks.  Every state array (906 MB) is larger
   than L2 (126 MB), so no explicit flush is needed.
+* N > 1 (torchrun): weak scaling by default (N copies of the mesh stacked
+  along the last axis, one decompose() block per rank, NCCL halos under the
+  interior elements); the line adds the sharded roofline (HBM time vs the
+  halo time at the measured NCCL/NVLink bandwidth) and run_scale rows
+  (src/experiments.cpp:306-399) against a 1-GPU run of the same mode.
 * e2e: the same metric through the reference-facing call with host buffers:
   upload (pinned host AoS -> device) + advance(K steps) + download, wall clock.
 * roofline: the fused stage kernel vs measured HBM bandwidth
@@ -134,6 +139,17 @@ def physical_cores() -> int:
     return os.cpu_count() or 1
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_cpu_reference(cfg_name: str, max_steps: int, warmup: int, budget_s: float = 30.0):
     """The reference's thread-parallel path (run_partitioned, partition.cpp:186-333)
     over the host's physical cores on the benchmark workload.  Steps are capped so
@@ -170,7 +186,22 @@ def run_cpu_reference(cfg_name: str, max_steps: int, warmup: int, budget_s: floa
               f"{'one untimed warm-up step' if kind == 'reference' else 'none'}; "
               f"{'run_partitioned' if workers > 1 else 'advance'} with {workers} worker thread(s)")
     return {"value": value, "unit": UNIT, "cores": workers, "kind": kind, "sample": sample,
-            "seconds": st.wall_seconds, "steps": st.steps}
+            "seconds": st.wall_seconds, "steps": st.steps, "cpu_model": cpu_model(),
+            "logical_cpus": os.cpu_count()}
+
+
+def run_cpu_serial(cfg_name: str, cells_per_axis: int = 96, steps: int = 2):
+    """The reference's serial advance (P = 1, src/solver.cpp:372-440) on a reduced
+    mesh of the same configuration (BASELINE.md §2 asks for the serial figure)."""
+    dim, cells, order, eq, rk, desc = CONFIGS[cfg_name]
+    ol, orc, kind = reference_lib()
+    small = tuple(min(c, cells_per_axis) for c in cells)
+    p = ol.Problem(dim, small, order, ol.EULER if eq else ol.ADVECTION, rk)
+    u0 = orc.initial(p)
+    _, st = orc.advance(p, u0, steps, True)
+    return {"value": p.size * STAGES[rk] * st.steps / st.wall_seconds, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"serial advance, {steps} steps after one warm-up, {'x'.join(map(str, small))} cells "
+                      f"({p.size} DOF) of the same equation/order/RK"}
 
 
 def bench_reference_arm(args):
@@ -194,6 +225,55 @@ def bench_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+L2_NOTE = {
+    "c2": "no flush: one RK4 step streams u and the K_j (5 arrays of 77 MB = 385 MB) through the 126 MB L2",
+    "c3": "no flush needed: each state array (906 MB) exceeds the 126 MB L2",
+    "c4": "no flush needed: each state array (4.3 GB) exceeds the 126 MB L2",
+    "c5": "no flush needed: each state array (6.4 GB / N GPUs) exceeds the 126 MB L2",
+}
+
+
+def link_probe(plan, dev, iters: int = 20):
+    """NCCL point-to-point over NVLink between this rank and its neighbours
+    along the first split axis, through torch.distributed (the same transport
+    ndgx's halo exchange uses): the time of one exchange of the real halo
+    plane (send up, receive from below) and the per-direction bandwidth of a
+    256 MB message.  Every rank calls it (matched collectives)."""
+    import torch
+    import torch.distributed as dist
+    axes = [a for a in range(3) if plan.split[a]]
+    a = axes[0]
+    up, down = plan.nbr[a][1], plan.nbr[a][0]
+
+    def run(n):
+        snd = torch.ones(n, dtype=torch.float64, device=f"cuda:{dev}")
+        rcv = torch.empty_like(snd)
+
+        def once():
+            for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, snd, up), dist.P2POp(dist.irecv, rcv, down)]):
+                w.wait()
+        for _ in range(3):
+            once()
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            once()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / iters * 1e-3  # seconds per exchange
+
+    plane = int(plan.plane[a])
+    t_plane = run(plane)
+    big = 32 * 1024 * 1024  # 256 MB
+    t_big = run(big)
+    return {"axis": a, "plane_bytes": 8 * plane, "plane_exchange_ms": t_plane * 1e3,
+            "link_gbs": 8 * big / t_big / 1e9,
+            "how": "torch.distributed NCCL batch_isend_irecv to the split-axis neighbours, CUDA events, "
+                   f"mean of {iters}; link_gbs from a 256 MB message (per direction)"}
+
+
 def bench_ours(args):
     import torch
     import torch.distributed as dist
@@ -208,7 +288,8 @@ def bench_ours(args):
     dim, cells, order, eq, rk, desc = CONFIGS[args.config]
     arith = ndgx.ARITH_FAST if args.arith == "fast" else ndgx.ARITH_EXACT
     # weak scaling: every GPU owns the configuration's mesh; N GPUs stack N
-    # copies along the last axis (decompose() then gives slabs, one per rank)
+    # copies along the last axis (decompose() then gives slabs, one per rank;
+    # run_scale's lowest-interface weak mesh, src/experiments.cpp:353-380)
     gcells = list(cells)
     if not args.strong:
         gcells[dim - 1] *= world
@@ -230,8 +311,10 @@ def bench_ours(args):
     else:
         s = ndgx.Solver(cfg, device=dev, arith=arith)
         lo, hi = (0, 0, 0), tuple(mesh.cells)
+    plan = s.plan
     dof = s.dof  # this rank's block
     dof_total = mesh.dof(model)  # all ranks (weak: world * dof; strong: the configuration's mesh)
+    exchanging = any(plan.split[a] for a in range(3))
 
     # pinned host state (the reference AoS layout), synthetic IC of this block
     host = torch.empty(dof, dtype=torch.float64, pin_memory=True)
@@ -248,9 +331,16 @@ def bench_ours(args):
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     s.upload_ptr(host.data_ptr())
     # warm-up: W untimed steps (graph capture, clocks)
-    s.launch_steps(max(args.warmup, 3) if args.warmup >= 3 else 3)
+    s.launch_steps(max(args.warmup, 3))
     s.sync()
     s.upload_ptr(host.data_ptr())
 
@@ -260,21 +350,12 @@ def bench_ours(args):
         s.launch_steps(args.steps)
         st = s.sync()
     barrier()
-    t_dev = st.wall_seconds
-    if world > 1:
-        t = torch.tensor([t_dev], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_dev = float(t.item())
+    t_dev = max_over_ranks(st.wall_seconds)
     value = dof_total * stages * args.steps / t_dev
 
-    # ---- kernel-level timing for the roofline (events around each stage) ----
-    stage_ms = []
-    ctl_ms = []
-    for _ in range(5):
-        ms, c = s.profile_step()
-        stage_ms.append(ms)
-        ctl_ms.append(c)
-    stage_ms = np.array(stage_ms[1:]).mean(axis=0)  # drop the first
+    # ---- per-stage timing inside the replayed step graph (globaltimer stamps) ----
+    stage_ms, ctl_ms = s.profile_step()
+    stage_ms = np.array(stage_ms)
     avg_stage_ms = float(stage_ms.mean())
     bytes_per_launch = BYTES_PER_DOF_STAGE[rk] * dof
     peak, peak_src = measured_peaks()
@@ -283,9 +364,25 @@ def bench_ours(args):
     prof_path = os.path.join(ROOT, "profiles", "ncu_stage_traffic.json")
     if os.path.exists(prof_path):
         with open(prof_path) as f:
-            tr = json.load(f).get(args.config, {}).get(args.arith)
+            prof = json.load(f)
+        tr = prof.get(args.config, {}).get(args.arith)
         if tr:
             traffic = tr.get("dram_bytes_per_launch")
+
+    # ---- sharded roofline (N > 1): HBM time vs halo time over NVLink ----
+    sharded = None
+    if world > 1 and exchanging:
+        lp = link_probe(plan, dev)
+        halo_bytes = sum(2 * 8 * int(plan.plane[a]) for a in range(3) if plan.split[a])
+        t_hbm = bytes_per_launch / (peak * 1e9)
+        t_halo = halo_bytes / (lp["link_gbs"] * 1e9)
+        lp_max = {k: max_over_ranks(v) if isinstance(v, float) else v for k, v in lp.items()}
+        sharded = {"halo_bytes_per_stage_per_gpu": halo_bytes, "hbm_bytes_per_stage_per_gpu": bytes_per_launch,
+                   "t_hbm_ms": t_hbm * 1e3, "t_halo_bw_ms": t_halo * 1e3,
+                   "t_halo_exchange_measured_ms": lp_max["plane_exchange_ms"],
+                   "link_gbs_measured": lp["link_gbs"], "bound": "hbm" if t_hbm >= t_halo else "nvlink",
+                   "stage_roofline_ms": max(t_hbm, t_halo) * 1e3, "probe": lp_max["how"],
+                   "note": "the halo exchange runs on the comm stream under the interior elements"}
 
     # ---- end-to-end through the reference-facing call (host buffers) ----
     barrier()
@@ -294,11 +391,7 @@ def bench_ours(args):
     st_e = s.advance(ndgx.StepPlan(args.steps, False))
     s.download_ptr(host.data_ptr())
     barrier()
-    t_e2e = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([t_e2e], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_e2e = float(t.item())
+    t_e2e = max_over_ranks(time.perf_counter() - t0)
     e2e = dof_total * stages * st_e.steps / t_e2e
     s.close()
 
@@ -321,25 +414,58 @@ def bench_ours(args):
         sx.launch_steps(args.steps)
         stx = sx.sync()
         barrier()
-        tx = stx.wall_seconds
-        if world > 1:
-            t = torch.tensor([tx], dtype=torch.float64, device=f"cuda:{dev}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            tx = float(t.item())
+        tx = max_over_ranks(stx.wall_seconds)
         exact = {"value": dof_total * stages * args.steps / tx, "unit": UNIT,
                  "ms_per_step": tx / args.steps * 1e3,
                  "note": "arith=exact: the reference's IEEE operation order, states bit-identical to the CPU reference"}
         sx.close()
 
+    # ---- run_scale rows (N > 1): the 1-GPU baseline of the same mode, on rank 0 ----
+    scale_rows = None
+    if world > 1 and not args.no_scale_baseline:
+        from paper_2510_05254_b200 import report as rp
+        base = None
+        if rank == 0:
+            # weak: one GPU with the per-GPU mesh; strong: one GPU with the whole mesh
+            bmesh = ndgx.Mesh(dim, tuple(cells), order)
+            bcfg = ndgx.SolverConfig(bmesh, model, rk, 0.4, 1.0)
+            hb = ndgx.init_euler_subsonic(bmesh, model) if eq else \
+                ndgx.init_multisine(bmesh, model, n_modes=40, seed=42)
+            with ndgx.Solver(bcfg, device=dev, arith=arith) as sb:
+                sb.upload(hb)
+                sb.launch_steps(3)
+                sb.sync()
+                sb.upload(hb)
+                sb.launch_steps(args.steps)
+                base = (bcfg, sb.sync())
+        barrier()
+        if rank == 0:
+            devname = torch.cuda.get_device_name(dev)
+            mode = "strong" if args.strong else "weak"
+            bcfg, bst = base
+            r1 = rp.scale_row(bcfg, bst, 1, devname, mode, note=f"ndgx {args.arith}, 1 GPU")
+            stats_n = ndgx.StepStats(st.steps, st.dt_min, st.dt_max, t_dev)
+            rn = rp.scale_row(cfg, stats_n, world, devname, mode,
+                              baseline_wall=bst.wall_seconds if args.strong else 0.0,
+                              baseline_tpd=0.0 if args.strong else r1.time_per_dof,
+                              note=f"ndgx {args.arith}, {world} GPUs, blocks {list(plan.grid)}")
+            scale_rows = [{c: rp._cell(r, c) for c in rp.COLUMNS} for r in (r1, rn)]
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             r = run_cpu_reference(args.config, max_steps=3, warmup=1, budget_s=20.0)
-            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "logical_cpus")}
+            cpu["serial_p1"] = run_cpu_serial(args.config)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
     if rank == 0:
+        # our kernels in the timed region: the first step's wavespeed scan (Euler),
+        # per step the step control and per stage one fused stage kernel (an
+        # exchanging block: pack + interior + boundary shell)
+        per_stage = 3 if exchanging else 1
+        launches = args.steps * (1 + stages * per_stage) + (1 if eq else 0)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
@@ -351,23 +477,29 @@ def bench_ours(args):
                                       "quadrature, <= 1e-12 relative L2 vs the reference (tests/test_gpu_parity.py); "
                                       "exact = bit-identical") ,
                        "parallelism": ("1 GPU" if not ranked else
-                                       f"{world} rank(s), decompose() blocks {list(s.plan.grid)}, NCCL face-halo "
-                                       f"exchange per RK stage" + (" (forced on every axis)" if args.force_exchange
-                                                                   else "")),
-                       "l2": "no flush needed: each state array (8*dof bytes) exceeds the 126 MB L2"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                                       f"{world} rank(s), decompose() blocks {list(plan.grid)}, NCCL face-halo "
+                                       f"exchange per RK stage on a comm stream under the interior elements" +
+                                       (" (forced on every axis)" if args.force_exchange else "")),
+                       "l2": L2_NOTE[args.config]},
+            "roofline": {"bound": sharded["bound"] if sharded else "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": "profiles/ncu_stage_traffic.json (ncu dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum per stage launch, same kernel), not this run",
                          "kernel": "ndgx::stage_kernel (fused NDG RHS + RK stage)",
                          "bytes_per_dof_stage": BYTES_PER_DOF_STAGE[rk],
-                         "avg_launch_ms": avg_stage_ms, "stage_ms": stage_ms.tolist(),
+                         "avg_launch_ms": avg_stage_ms, "stage_ms": stage_ms.tolist(), "step_control_ms": ctl_ms,
+                         "stage_timing": "globaltimer stamps between the stages of the replayed two-step graph "
+                                         "(steady state, one extra 1-thread launch per stage)",
                          "peak_source": peak_src,
-                         "step_frac": value / world * BYTES_PER_DOF_STAGE[rk] / 1e9 / peak},
+                         "step_frac": value / world * BYTES_PER_DOF_STAGE[rk] / 1e9 / peak,
+                         "sharded": sharded},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * dof / args.steps,
                     "d2h_bytes_per_step": 8 * dof / args.steps,
                     "note": "one advance(StepPlan{K}) call: pinned host AoS upload, K steps, download"},
             "exact_mode": exact,
-            "gpu_launches": args.steps * (1 + stages) + (1 if eq else 0),
+            "scale_rows": scale_rows,
+            "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -401,6 +533,8 @@ def main():
     ap.add_argument("--arith", default="fast", choices=["exact", "fast"])
     ap.add_argument("--no-exact-arm", action="store_true", help="skip the bit-exact side measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scale-baseline", action="store_true",
+                    help="N > 1: skip the 1-GPU baseline run behind the run_scale rows")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: the configuration's mesh is split across the N GPUs (C5) "
                          "instead of stacking N copies (weak scaling, the default)")

@@ -318,13 +318,13 @@ static __global__ void step_begin_kernel(StepParams sp) {
 }
 
 // ====================================================== in-graph timing
-// The global nanosecond timer into out[i]: launched between the stages of a
-// captured step, consecutive stamps bracket each stage exactly as it runs in
-// the timed graph (events recorded inside a graph cannot be timed).
-static __global__ void stamp_kernel(unsigned long long* out, int i) {
+// The global nanosecond timer into the next slot of out: launched between the
+// stages of captured steps, consecutive stamps bracket each stage as it runs
+// in the timed graph (events recorded inside a graph cannot be timed).
+static __global__ void stamp_kernel(unsigned long long* out, unsigned int* count) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  out[i] = t;
+  out[atomicAdd(count, 1u)] = t;
 }
 
 // ===================================================== layout permutation

@@ -1572,15 +1572,17 @@ int ndgx_sync(ndgx_solver* s, ndgx_stats* stats, ndgx_error* err) {
   }
 }
 
-// Per-kernel timing of one step: the step (step control + every stage) is
-// captured in a CUDA graph with a 1-thread %globaltimer stamp kernel between
-// the stages and replayed `reps` times, so the stages run back to back exactly
-// as in the timed graph.  ms[i] = mean time of stage i (a split stage's
-// interior and boundary shell end to end, plus one stamp launch);
-// ms[stages] = the step control (and a rank solver's wavespeed all-reduce).
+// Per-kernel timing in the steady state: two steps (the timed graph's unit)
+// are captured with a 1-thread %globaltimer stamp kernel before the step
+// control and after every stage, and the graph is replayed `reps` times back
+// to back.  ms[i] = mean time of stage i over all but the first replay (a
+// split stage's interior and boundary shell end to end, plus one stamp
+// launch); ms[stages] = the step control (and a rank solver's wavespeed
+// all-reduce).  Every step starts from the current state and writes the
+// scratch buffers, so the state is left unchanged.
 int ndgx_profile_step(ndgx_solver* s, float* ms, int n, ndgx_error* err) {
   clear_error(err);
-  const int reps = 5;
+  const int reps = 6, per = 2 * (s->stages + 1) + 1;  // stamps per replay
   cudaGraphExec_t exec = nullptr;
   unsigned long long* stamps = nullptr;
   try {
@@ -1589,39 +1591,48 @@ int ndgx_profile_step(ndgx_solver* s, float* ms, int n, ndgx_error* err) {
       set_error(err, NDGX_ERR_CONFIG, "profile_step needs the blocks on one device");
       return NDGX_ERR_CONFIG;
     }
-    const int ns = s->stages + 2;
-    ck(cudaMalloc(&stamps, ns * sizeof(unsigned long long)), "cudaMalloc stamps");
+    ck(cudaMalloc(&stamps, reps * per * sizeof(unsigned long long) + 16), "cudaMalloc stamps");
+    unsigned int* count = reinterpret_cast<unsigned int*>(stamps + reps * per);
+    ck(cudaMemsetAsync(count, 0, sizeof(unsigned int), s->stream()), "memset");
     cudaGraph_t g;
     ck(cudaStreamBeginCapture(s->stream(), s->comm ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal),
        "begin capture");
-    const StepParams sp = s->step_params(s->ctl_warm, 1, 0);
-    ndgx::stamp_kernel<<<1, 1, 0, s->stream()>>>(stamps, 0);
-    s->launch_alpha_reduce(s->ctl_warm);
-    ndgx::step_begin_kernel<<<1, 1, 0, s->stream()>>>(sp);
-    ndgx::stamp_kernel<<<1, 1, 0, s->stream()>>>(stamps, 1);
-    for (int i = 0; i < s->stages; ++i) {
-      s->fork();
-      s->launch_stage_all(i, s->parity, s->ctl_warm, false);
-      s->join();
-      ndgx::stamp_kernel<<<1, 1, 0, s->stream()>>>(stamps, 2 + i);
+    const StepParams sp = s->step_params(s->ctl_warm, 2LL * reps, 0);
+    s->xpar = 0;
+    for (int k = 0; k < 2; ++k) {
+      ndgx::stamp_kernel<<<1, 1, 0, s->stream()>>>(stamps, count);
+      s->launch_alpha_reduce(s->ctl_warm);
+      ndgx::step_begin_kernel<<<1, 1, 0, s->stream()>>>(sp);
+      for (int i = 0; i < s->stages; ++i) {
+        ndgx::stamp_kernel<<<1, 1, 0, s->stream()>>>(stamps, count);
+        s->fork();
+        s->launch_stage_all(i, s->parity, s->ctl_warm, false);  // both steps from u: u is never written
+        s->join();
+      }
     }
+    ndgx::stamp_kernel<<<1, 1, 0, s->stream()>>>(stamps, count);  // the end of the second step's last stage
     ck(cudaStreamEndCapture(s->stream(), &g), "end capture");
     ck(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
     cudaGraphDestroy(g);
-    std::vector<double> acc(s->stages + 1, 0.0);
-    std::vector<unsigned long long> h(ns);
-    for (int r = 0; r < reps + 1; ++r) {
-      s->reset_control(s->ctl_warm);
-      s->launch_scan(s->ctl_warm, s->parity);
-      ck(cudaGraphLaunch(exec, s->stream()), "graph");
-      ck(cudaMemcpyAsync(h.data(), stamps, ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->stream()),
-         "stamps");
-      ck(cudaStreamSynchronize(s->stream()), "sync");
-      if (r == 0) continue;  // the first replay uploads the graph
-      for (int i = 0; i < s->stages; ++i) acc[i] += (double)(h[2 + i] - h[1 + i]) * 1e-6;
-      acc[s->stages] += (double)(h[1] - h[0]) * 1e-6;
-    }
-    for (int i = 0; i <= s->stages && i < n; ++i) ms[i] = (float)(acc[i] / reps);
+    s->reset_control(s->ctl_warm);
+    s->launch_scan(s->ctl_warm, s->parity);
+    for (int r = 0; r < reps; ++r) ck(cudaGraphLaunch(exec, s->stream()), "graph");
+    std::vector<unsigned long long> h((size_t)reps * per);
+    ck(cudaMemcpyAsync(h.data(), stamps, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->stream()),
+       "stamps");
+    ck(cudaStreamSynchronize(s->stream()), "sync");
+    // per replay: [before ctl, before stage 0 .. before stage S-1] x 2 steps, then a closing stamp
+    const int w = s->stages + 1;
+    std::vector<double> acc(w, 0.0);
+    int cnt = 0;
+    for (int r = 1; r < reps; ++r)
+      for (int k = 0; k < 2; ++k) {
+        const size_t b0 = (size_t)r * per + (size_t)k * w;
+        for (int i = 0; i < s->stages; ++i) acc[i] += (double)(h[b0 + 2 + i] - h[b0 + 1 + i]) * 1e-6;
+        acc[s->stages] += (double)(h[b0 + 1] - h[b0]) * 1e-6;
+        ++cnt;
+      }
+    for (int i = 0; i <= s->stages && i < n; ++i) ms[i] = (float)(acc[i] / cnt);
     cudaGraphExecDestroy(exec);
     cudaFree(stamps);
   } catch (const CudaFailure& f) {

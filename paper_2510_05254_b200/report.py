@@ -129,3 +129,19 @@ def timing_row(cfg, stats, workers: int, device: str, experiment: str = "timing"
     row.wall_seconds = stats.wall_seconds
     row.time_per_dof = stats.wall_seconds / float(row.dof)
     return row
+
+
+def scale_row(cfg, stats, workers: int, device: str, mode: str, baseline_wall: float = 0.0,
+              baseline_tpd: float = 0.0, note: str = "") -> BenchRow:
+    """One run_scale row (src/experiments.cpp:306-399): base_row + fill_stats
+    with note = mode ("strong" / "weak"); a strong row against the serial
+    baseline's wall time gets speedup = baseline_wall / wall and efficiency =
+    speedup / workers, a weak row efficiency = baseline_tpd / time_per_dof
+    (baseline = the 1-worker row of the same mode)."""
+    row = timing_row(cfg, stats, workers, device, experiment="scale", note=mode + (f" ({note})" if note else ""))
+    if baseline_wall > 0.0:
+        row.speedup = baseline_wall / row.wall_seconds
+        row.efficiency = row.speedup / workers
+    if baseline_tpd > 0.0:
+        row.efficiency = baseline_tpd / row.time_per_dof
+    return row
