@@ -287,10 +287,15 @@ struct Lane4 {
   double k[3];  // K_d[r][c] (0 for r >= 4)
 };
 
-template <int KIND, int NU, int AM, int BM>
+// Runs (RA = 0: x, 2: z; -1: none): a warp visiting consecutive elements
+// along axis RA reuses the previous element's hi-face flux as this
+// element's lo-face flux (`prev`): the two face-flux slots of that axis
+// alternate with `par`, so the hi slot of one element is the lo slot of the
+// next.  Bitwise the same value: LF(U-, U+) of the same two stage inputs.
+template <int KIND, int NU, int AM, int BM, int RA = -1>
 __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4& ln, int lane, int e, int cx,
                                                  int cy, int cz, double* sF, double* sT, double* sH, double dt,
-                                                 long long step, double& alpha) {
+                                                 long long step, double& alpha, bool prev = false, int par = 0) {
   constexpr int N = 4, NPE = 64, L = 16, DIM = 3;
   constexpr int NV = KIND == 0 ? 1 : 4;
   constexpr int TW = NV + 1;  // trace record: U (+1 spare slot); flux and speed are recomputed at the face
@@ -387,11 +392,13 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
   __syncwarp();
 
   // ---------------------------------------------------------- faces (96 nodes, 3 per lane)
+  // iteration m: axis d = m, lanes 0-15 the lo face, 16-31 the hi face
 #pragma unroll
   for (int m = 0; m < 3; ++m) {
-    const int q = lane + 32 * m;
-    const int f = q >> 4, t = q & 15;
-    const int d = f >> 1, side = f & 1;
+    const int d = m, side = lane >> 4, t = lane & 15;
+    const int f = 2 * d + side;                              // trace slot
+    const int fh = 2 * d + (d == RA ? (side ^ par) : side);  // face-flux slot
+    if (d == RA && prev && side == 0) continue;              // the previous element's hi-face flux
     const int ca = d == 0 ? cx : (d == 1 ? cy : cz);
     const int cn = d == 0 ? C0 : (d == 1 ? C1 : C2);
     const bool bnd = side ? (ca == cn - 1) : (ca == 0);
@@ -436,7 +443,9 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
       // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
       const double um = side ? Uo[v] : Un[v], up = side ? Un[v] : Uo[v];
       const double fm = side ? Fo[v] : Fn[v], fp = side ? Fn[v] : Fo[v];
-      sH[(f * NV + v) * L + t] = 0.5 * ((fm + fp) - al * (up - um));
+      // explicit roundings: every code path (either side, run or not) gives
+      // the same bits, so a reused hi-face flux equals a recomputed lo one
+      sH[(fh * NV + v) * L + t] = __dmul_rn(0.5, fma(-al, __dsub_rn(up, um), __dadd_rn(fm, fp)));
     }
   }
   __syncwarp();
@@ -473,12 +482,14 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
           for (int s2 = 0; s2 < 2; ++s2) {
             const int n = s2 ? o1 : o0;
             const int i = n & 3, j = (n >> 2) & 3, kk = n >> 4;
-            if (i == 0) dv[s2] = fma(p.lift[0], sH[(0 * NV + v) * L + j + 4 * kk], dv[s2]);
-            if (i == N - 1) dv[s2] = fma(-p.lift[0], sH[(1 * NV + v) * L + j + 4 * kk], dv[s2]);
-            if (j == 0) dv[s2] = fma(p.lift[1], sH[(2 * NV + v) * L + i + 4 * kk], dv[s2]);
-            if (j == N - 1) dv[s2] = fma(-p.lift[1], sH[(3 * NV + v) * L + i + 4 * kk], dv[s2]);
-            if (kk == 0) dv[s2] = fma(p.lift[2], sH[(4 * NV + v) * L + i + 4 * j], dv[s2]);
-            if (kk == N - 1) dv[s2] = fma(-p.lift[2], sH[(5 * NV + v) * L + i + 4 * j], dv[s2]);
+            constexpr int X0 = 0, Y0 = 2, Z0 = 4;
+            const int xl = X0 + (RA == 0 ? par : 0), zl = Z0 + (RA == 2 ? par : 0);  // run-axis slots alternate
+            if (i == 0) dv[s2] = fma(p.lift[0], sH[(xl * NV + v) * L + j + 4 * kk], dv[s2]);
+            if (i == N - 1) dv[s2] = fma(-p.lift[0], sH[((2 * X0 + 1 - xl) * NV + v) * L + j + 4 * kk], dv[s2]);
+            if (j == 0) dv[s2] = fma(p.lift[1], sH[(Y0 * NV + v) * L + i + 4 * kk], dv[s2]);
+            if (j == N - 1) dv[s2] = fma(-p.lift[1], sH[((Y0 + 1) * NV + v) * L + i + 4 * kk], dv[s2]);
+            if (kk == 0) dv[s2] = fma(p.lift[2], sH[(zl * NV + v) * L + i + 4 * j], dv[s2]);
+            if (kk == N - 1) dv[s2] = fma(-p.lift[2], sH[((2 * Z0 + 1 - zl) * NV + v) * L + i + 4 * j], dv[s2]);
           }
           const double k0 = dv[0] * dt, k1 = dv[1] * dt;
           double* gout = p.out + ebase + v * NPE + o0;  // o1 == o0 + 1
@@ -996,8 +1007,234 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       e = nelem;  // done: skip the element loop below
     }
   }
-  for (; e < nelem; e += es) {
+  // the generic body (exact mode, and the contracted shapes without a tensor-core body)
+  auto generic_element = [&](const int e, const int cx, const int cy, const int cz, const double* src,
+                             const double* fsrc) {
     const size_t ebase = (size_t)e * NV * NPE;
+      auto aos_cell = [&]() -> long long {  // global AoS cell index of this element
+        const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
+        return (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz;
+      };
+
+      // ------------------------------------------------ 1: nodes
+      // lane's nodes: n = lane + 32m
+      double Sn[G::NM][NV];  // last stage: S at the lane's nodes
+  #pragma unroll
+      for (int m = 0; m < G::NM; ++m) {
+        const int n = lane + 32 * m;
+        if (n >= NPE) continue;
+        double U[NV];
+  #pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double S;
+          if (depth > 0)
+            combine_s<EXACT, NU, AM, BM>(p, src + v * NPE + n, G::CHUNK, last, U[v], S);
+          else
+            combine_g<EXACT, NU, AM, BM>(p, ebase + (size_t)v * NPE + n, last, U[v], S);
+          Sn[m][v] = S;
+        }
+        if (KIND == 1 && !(U[0] > 0.0)) {
+          // first bad node of the reference's x-volume traversal: (cell, (j,k), i)
+          const int i = n % N, j = (n / N) % N, k = n / (N * N);
+          const int nkey = (DIM == 2) ? j * N + i : (j * N + k) * N + i;
+          record_error(ctl, error_key(step, p.phase, aos_cell(), nkey));
+        }
+        const double rinv = (!EXACT && KIND == 1) ? fast_rcp(U[0]) : -1.0;
+  #pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          double F[NV], sp;
+          flux<DIM, KIND, EXACT>(p, U, d, F, sp, rinv);
+  #pragma unroll
+          for (int v = 0; v < NV; ++v) sF[(d * NV + v) * NPE + n] = F[v];
+          const int k = G::pos_of(d, n);
+          if (k == 0 || k == N - 1) {
+            double* t = sT + ((2 * d + (k == 0 ? 0 : 1)) * HW) * L + G::line_of(d, n);
+  #pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              t[v * L] = U[v];
+              if (!GEN_UTRACE) t[(NV + v) * L] = F[v];
+            }
+            if (!GEN_UTRACE) t[2 * NV * L] = sp;
+          }
+        }
+      }
+      __syncwarp();
+
+      // ------------------------------------------------ 2: face fluxes
+  #pragma unroll
+      for (int m = 0; m < G::FM; ++m) {
+        const int q = lane + 32 * m;
+        if (q >= G::FN) continue;
+        const int f = q / L, t = q - f * L;
+        const int d = f >> 1, side = f & 1;
+        const double* own = sT + (f * HW) * L + t;
+        // neighbour across (d, side): periodic wrap in this block, or the received plane
+        const int ca = d == 0 ? cx : (d == 1 ? cy : cz);
+        const int cn = d == 0 ? C0 : (d == 1 ? C1 : C2);
+        const bool boundary = side ? (ca == cn - 1) : (ca == 0);
+        double Un[NV];
+        if (G::FACE_PF && depth > 0) {
+          const bool ext = boundary && p.ext[d][side] != nullptr;
+  #pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            double S;
+            if (ext) Un[v] = fsrc[v * 32 + lane];
+            else combine_s<EXACT, NU, AM, BM>(p, fsrc + v * 32 + lane, NV * 32, false, Un[v], S);
+          }
+        } else if (boundary && p.ext[d][side] != nullptr) {
+          const size_t xs = d == 0 ? (size_t)cy + (size_t)C1 * cz
+                                   : (d == 1 ? (size_t)cx + (size_t)C0 * cz : (size_t)cx + (size_t)C0 * cy);
+  #pragma unroll
+          for (int v = 0; v < NV; ++v) Un[v] = __ldg(p.ext[d][side] + (xs * NV + v) * L + t);
+        } else {
+          // neighbour element index: e -/+ stride_d, wrapped periodically
+          const int stride = d == 0 ? 1 : (d == 1 ? C0 : C0 * C1);
+          const int en = side ? (ca + 1 == cn ? e - (cn - 1) * stride : e + stride)
+                              : (ca == 0 ? e + (cn - 1) * stride : e - stride);
+          const size_t g = (size_t)en * (NV * NPE) + G::node(d, t, side ? 0 : N - 1);
+  #pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            double S;
+            combine_g<EXACT, NU, AM, BM>(p, g + (size_t)v * NPE, false, Un[v], S);
+          }
+        }
+        double Fn[NV], sn;
+        flux<DIM, KIND, EXACT>(p, Un, d, Fn, sn, (!EXACT && KIND == 1) ? fast_rcp(Un[0]) : -1.0);
+        // this element's side: U from the trace, flux and speed recomputed
+        // (the same function of the same U as in the node phase)
+        double Uo[NV], Fo[NV], so;
+  #pragma unroll
+        for (int v = 0; v < NV; ++v) Uo[v] = own[v * L];
+        if (GEN_UTRACE) {
+          flux<DIM, KIND, EXACT>(p, Uo, d, Fo, so, (!EXACT && KIND == 1) ? fast_rcp(Uo[0]) : -1.0);
+        } else {
+  #pragma unroll
+          for (int v = 0; v < NV; ++v) Fo[v] = own[(NV + v) * L];
+          so = own[2 * NV * L];
+        }
+        const double a = dmax(side ? so : sn, side ? sn : so);
+  #pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
+          const double um = side ? Uo[v] : Un[v], up = side ? Un[v] : Uo[v];
+          const double fm = side ? Fo[v] : Fn[v], fp = side ? Fn[v] : Fo[v];
+          sH[(f * NV + v) * L + t] = A::mul(0.5, A::sub(A::add(fm, fp), A::mul(a, A::sub(up, um))));
+        }
+      }
+      __syncwarp();
+
+      // ------------------------------------------------ 3: volume, faces, epilogue
+  #pragma unroll
+      for (int m = 0; m < G::NM; ++m) {
+        const int n = lane + 32 * m;
+        if (n >= NPE) continue;
+        double un[NV];
+  #pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double D = 0.0;
+  #pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            const int k = G::pos_of(d, n), t = G::line_of(d, n);
+            const double* Fl = sF + (d * NV + v) * NPE;
+            const double* Kr = &p.K[d][k * N];
+            // 0 + K0 F0 + K1 F1 + ...: the leading 0 + only normalises a -0,
+            // which zero_plus (axis 0) or the add onto dudt (axes > 0) reproduces
+            double acc = A::mul(Kr[0], Fl[G::node(d, t, 0)]);
+  #pragma unroll
+            for (int l = 1; l < N; ++l) acc = A::mac(acc, Kr[l], Fl[G::node(d, t, l)]);
+            D = d == 0 ? zero_plus(acc) : A::add(D, acc);
+            if (k == 0) D = A::add(D, A::mul(p.lift[d], sH[((2 * d) * NV + v) * L + t]));
+            if (k == N - 1) D = A::sub(D, A::mul(p.lift[d], sH[((2 * d + 1) * NV + v) * L + t]));
+          }
+          const size_t gi = ebase + (size_t)v * NPE + n;
+          const double kv = A::mul(D, dt);  // k_i *= dt (solver.hpp:66-67)
+          if (!last) {
+            p.out[gi] = kv;
+          } else {
+            un[v] = p.b_last != 0.0 ? A::mac(Sn[m][v], p.b_last, kv) : Sn[m][v];
+            p.out[gi] = un[v];
+          }
+        }
+        if (last) {
+          bool fin = true;
+  #pragma unroll
+          for (int v = 0; v < NV; ++v) fin = fin && isfinite(un[v]);
+          if (!fin) record_error(ctl, error_key(step, kPhaseInstability, p.block_id, 0));
+          if (KIND == 1 && p.scan_alpha) {
+            if (!(un[0] > 0.0)) {
+              record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(), G::aos_node(n)));
+            } else {
+              double mm = 0.0;
+  #pragma unroll
+              for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[1 + d]));
+              alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[0]), p.sound_speed));
+            }
+          }
+        }
+      }
+    __syncwarp();  // this element's slab reads precede the next element's writes
+  };
+
+
+#ifndef NDGX_RUN3
+#define NDGX_RUN3 2  // 3D traversal of whole-plane launches: 0 element order, 1 x-runs, 2 z-runs
+#endif
+#ifndef NDGX_RUNLEN3
+#define NDGX_RUNLEN3 16
+#endif
+#ifndef NDGX_YB3
+#define NDGX_YB3 8
+#endif
+#ifndef NDGX_REUSE3
+#define NDGX_REUSE3 1
+#endif
+  // 3D: runs of consecutive elements along z (x-runs: along x, in y-blocks of
+  // NDGX_YB3 rows) per warp.  In element order (x fastest) the z neighbour
+  // is C0*C1 elements away and, at the many-term RK6 stages, falls out of L2
+  // before it is read again (C4 stage 5: 1.5x the compulsory DRAM bytes).
+  // In a z-run the z neighbours are this warp's previous and next elements,
+  // and the tensor-core body takes the lo-face flux from the previous one.
+  if constexpr (DIM == 3 && NDGX_RUN3 != 0) {
+    const int plane = C0 * C1;
+    if (depth == 0 && e_stride == 1 && p.region == 0 && e_lo % plane == 0 && nelem % plane == 0 && nelem > e_lo) {
+      const int z0 = e_lo / plane, nz = nelem / plane - z0;
+      const int w0 = (int)blockIdx.x * G::WARPS + wib;
+      auto visit = [&](int x, int y, int z, bool prev, int par) {
+        const int ee = x + C0 * (y + C1 * z);
+        if constexpr (USE_MMA3)
+          element_3d4_fast<KIND, NU, AM, BM, NDGX_RUN3 == 2 ? 2 : 0>(p, ln4, lane, ee, x, y, z, sF, sT, sH, dt, step,
+                                                                    alpha, NDGX_REUSE3 != 0 && prev, par);
+        else
+          generic_element(ee, x, y, z, nullptr, nullptr);
+      };
+      if (NDGX_RUN3 == 2) {
+        const int ZR = nz < NDGX_RUNLEN3 ? nz : NDGX_RUNLEN3;
+        const int nzc = (nz + ZR - 1) / ZR;
+        for (int rho = w0; rho < plane * nzc; rho += nw) {
+          const int zc = rho / plane, xy = rho - zc * plane;
+          const int y = xy / C0, x = xy - y * C0;
+          const int zb = z0 + zc * ZR, ze = min(zb + ZR, z0 + nz);
+          for (int z = zb; z < ze; ++z) visit(x, y, z, z > zb, (z - zb) & 1);
+        }
+      } else {
+        const int XR = C0 < NDGX_RUNLEN3 ? C0 : NDGX_RUNLEN3;
+        const int nxc = (C0 + XR - 1) / XR;
+        const int YB = (C1 % NDGX_YB3 == 0) ? NDGX_YB3 : C1;
+        const int nruns = nxc * C1 * nz;
+        for (int rho = w0; rho < nruns; rho += nw) {
+          int q = rho / nxc;
+          const int xc = rho - q * nxc;
+          const int yy = q % YB;
+          q /= YB;
+          const int z = z0 + q % nz, yb = q / nz;
+          const int y = yb * YB + yy, xb = xc * XR, xe = min(xb + XR, C0);
+          for (int x = xb; x < xe; ++x) visit(x, y, z, x > xb, (x - xb) & 1);
+        }
+      }
+      e = nelem;  // done: skip the element loop below
+    }
+  }
+  for (; e < nelem; e += es) {
     const double* src = ring + slot * SLOT;  // this element's u and K_j (when depth > 0)
     const double* fsrc = src + (1 + NU) * G::CHUNK;  // its face neighbour values (FACE_PF)
     if (depth > 0) {
@@ -1041,168 +1278,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       step_coords(cx, cy, cz);
       continue;
     }
-    auto aos_cell = [&]() -> long long {  // global AoS cell index of this element
-      const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
-      return (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz;
-    };
-
-    // ------------------------------------------------ 1: nodes
-    // lane's nodes: n = lane + 32m
-    double Sn[G::NM][NV];  // last stage: S at the lane's nodes
-#pragma unroll
-    for (int m = 0; m < G::NM; ++m) {
-      const int n = lane + 32 * m;
-      if (n >= NPE) continue;
-      double U[NV];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        double S;
-        if (depth > 0)
-          combine_s<EXACT, NU, AM, BM>(p, src + v * NPE + n, G::CHUNK, last, U[v], S);
-        else
-          combine_g<EXACT, NU, AM, BM>(p, ebase + (size_t)v * NPE + n, last, U[v], S);
-        Sn[m][v] = S;
-      }
-      if (KIND == 1 && !(U[0] > 0.0)) {
-        // first bad node of the reference's x-volume traversal: (cell, (j,k), i)
-        const int i = n % N, j = (n / N) % N, k = n / (N * N);
-        const int nkey = (DIM == 2) ? j * N + i : (j * N + k) * N + i;
-        record_error(ctl, error_key(step, p.phase, aos_cell(), nkey));
-      }
-      const double rinv = (!EXACT && KIND == 1) ? fast_rcp(U[0]) : -1.0;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        double F[NV], sp;
-        flux<DIM, KIND, EXACT>(p, U, d, F, sp, rinv);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) sF[(d * NV + v) * NPE + n] = F[v];
-        const int k = G::pos_of(d, n);
-        if (k == 0 || k == N - 1) {
-          double* t = sT + ((2 * d + (k == 0 ? 0 : 1)) * HW) * L + G::line_of(d, n);
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            t[v * L] = U[v];
-            if (!GEN_UTRACE) t[(NV + v) * L] = F[v];
-          }
-          if (!GEN_UTRACE) t[2 * NV * L] = sp;
-        }
-      }
-    }
-    __syncwarp();
-
-    // ------------------------------------------------ 2: face fluxes
-#pragma unroll
-    for (int m = 0; m < G::FM; ++m) {
-      const int q = lane + 32 * m;
-      if (q >= G::FN) continue;
-      const int f = q / L, t = q - f * L;
-      const int d = f >> 1, side = f & 1;
-      const double* own = sT + (f * HW) * L + t;
-      // neighbour across (d, side): periodic wrap in this block, or the received plane
-      const int ca = d == 0 ? cx : (d == 1 ? cy : cz);
-      const int cn = d == 0 ? C0 : (d == 1 ? C1 : C2);
-      const bool boundary = side ? (ca == cn - 1) : (ca == 0);
-      double Un[NV];
-      if (G::FACE_PF && depth > 0) {
-        const bool ext = boundary && p.ext[d][side] != nullptr;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double S;
-          if (ext) Un[v] = fsrc[v * 32 + lane];
-          else combine_s<EXACT, NU, AM, BM>(p, fsrc + v * 32 + lane, NV * 32, false, Un[v], S);
-        }
-      } else if (boundary && p.ext[d][side] != nullptr) {
-        const size_t xs = d == 0 ? (size_t)cy + (size_t)C1 * cz
-                                 : (d == 1 ? (size_t)cx + (size_t)C0 * cz : (size_t)cx + (size_t)C0 * cy);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) Un[v] = __ldg(p.ext[d][side] + (xs * NV + v) * L + t);
-      } else {
-        // neighbour element index: e -/+ stride_d, wrapped periodically
-        const int stride = d == 0 ? 1 : (d == 1 ? C0 : C0 * C1);
-        const int en = side ? (ca + 1 == cn ? e - (cn - 1) * stride : e + stride)
-                            : (ca == 0 ? e + (cn - 1) * stride : e - stride);
-        const size_t g = (size_t)en * (NV * NPE) + G::node(d, t, side ? 0 : N - 1);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double S;
-          combine_g<EXACT, NU, AM, BM>(p, g + (size_t)v * NPE, false, Un[v], S);
-        }
-      }
-      double Fn[NV], sn;
-      flux<DIM, KIND, EXACT>(p, Un, d, Fn, sn, (!EXACT && KIND == 1) ? fast_rcp(Un[0]) : -1.0);
-      // this element's side: U from the trace, flux and speed recomputed
-      // (the same function of the same U as in the node phase)
-      double Uo[NV], Fo[NV], so;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) Uo[v] = own[v * L];
-      if (GEN_UTRACE) {
-        flux<DIM, KIND, EXACT>(p, Uo, d, Fo, so, (!EXACT && KIND == 1) ? fast_rcp(Uo[0]) : -1.0);
-      } else {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) Fo[v] = own[(NV + v) * L];
-        so = own[2 * NV * L];
-      }
-      const double a = dmax(side ? so : sn, side ? sn : so);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
-        const double um = side ? Uo[v] : Un[v], up = side ? Un[v] : Uo[v];
-        const double fm = side ? Fo[v] : Fn[v], fp = side ? Fn[v] : Fo[v];
-        sH[(f * NV + v) * L + t] = A::mul(0.5, A::sub(A::add(fm, fp), A::mul(a, A::sub(up, um))));
-      }
-    }
-    __syncwarp();
-
-    // ------------------------------------------------ 3: volume, faces, epilogue
-#pragma unroll
-    for (int m = 0; m < G::NM; ++m) {
-      const int n = lane + 32 * m;
-      if (n >= NPE) continue;
-      double un[NV];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        double D = 0.0;
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-          const int k = G::pos_of(d, n), t = G::line_of(d, n);
-          const double* Fl = sF + (d * NV + v) * NPE;
-          const double* Kr = &p.K[d][k * N];
-          // 0 + K0 F0 + K1 F1 + ...: the leading 0 + only normalises a -0,
-          // which zero_plus (axis 0) or the add onto dudt (axes > 0) reproduces
-          double acc = A::mul(Kr[0], Fl[G::node(d, t, 0)]);
-#pragma unroll
-          for (int l = 1; l < N; ++l) acc = A::mac(acc, Kr[l], Fl[G::node(d, t, l)]);
-          D = d == 0 ? zero_plus(acc) : A::add(D, acc);
-          if (k == 0) D = A::add(D, A::mul(p.lift[d], sH[((2 * d) * NV + v) * L + t]));
-          if (k == N - 1) D = A::sub(D, A::mul(p.lift[d], sH[((2 * d + 1) * NV + v) * L + t]));
-        }
-        const size_t gi = ebase + (size_t)v * NPE + n;
-        const double kv = A::mul(D, dt);  // k_i *= dt (solver.hpp:66-67)
-        if (!last) {
-          p.out[gi] = kv;
-        } else {
-          un[v] = p.b_last != 0.0 ? A::mac(Sn[m][v], p.b_last, kv) : Sn[m][v];
-          p.out[gi] = un[v];
-        }
-      }
-      if (last) {
-        bool fin = true;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) fin = fin && isfinite(un[v]);
-        if (!fin) record_error(ctl, error_key(step, kPhaseInstability, p.block_id, 0));
-        if (KIND == 1 && p.scan_alpha) {
-          if (!(un[0] > 0.0)) {
-            record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(), G::aos_node(n)));
-          } else {
-            double mm = 0.0;
-#pragma unroll
-            for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[1 + d]));
-            alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[0]), p.sound_speed));
-          }
-        }
-      }
-    }
-    __syncwarp();  // this element's slab reads precede the next element's writes
+    generic_element(e, cx, cy, cz, src, fsrc);
     if (depth > 0 && ++slot == depth) {
       slot = 0;
       parity ^= 1;

@@ -28,8 +28,22 @@ for inst in dims:
         ["-c", os.path.join(b.CSRC, "ndgx_inst.cu"), "-o", obj]
     subprocess.run(cmd, check=True)
     objs = [o for o in objs if os.path.basename(o) != tag + ".o"] + [obj]
-subprocess.run([b.NVCC] + b.ARCH + ["-shared", "-o", os.path.join(out, "libndgx.so")] + objs + ["-lpthread", "-ldl"],
+# slim library: the other instances are stubs returning "not compiled" (small
+# enough to ship to the GPU box next to the others)
+keep = {f"ndgx_inst_d{i.split(',')[0]}_o{i.split(',')[1]}_e{i.split(',')[2]}" for i in dims}
+stub = os.path.join(out, "stubs.cu")
+with open(stub, "w") as f:
+    f.write('#include "ndgx_kernels.h"\nnamespace ndgx {\n')
+    for d in (1, 2, 3):
+        for n in range(2, 9):
+            for e in (0, 1):
+                if f"ndgx_inst_d{d}_o{n}_e{e}" not in keep:
+                    f.write(f"StageKernel NDGX_ENTRY_NAME({d}, {n}, {e})(int) {{ return StageKernel{{}}; }}\n")
+    f.write("}\n")
+subprocess.run([b.NVCC] + b.ARCH + b.FLAGS + ["-c", stub, "-o", stub + ".o"], check=True)
+objs = [o for o in objs if not os.path.basename(o).startswith("ndgx_inst_") or os.path.basename(o)[:-2] in keep]
+subprocess.run([b.NVCC] + b.ARCH + ["-shared", "-o", os.path.join(out, "libndgx.so")] + objs + [stub + ".o", "-lpthread", "-ldl"],
                check=True)
-for o in glob.glob(os.path.join(out, "*.o")):
+for o in glob.glob(os.path.join(out, "*.o")) + [stub]:
     os.remove(o)
 print(os.path.join(out, "libndgx.so"))
