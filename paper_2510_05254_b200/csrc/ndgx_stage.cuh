@@ -41,13 +41,13 @@
 
 namespace ndgx {
 
-// Stage signatures (kSigs index) that take the 3D order-4 tensor-core body,
-// as measured at 128^3 cells: the u-only and one-term stages and the last
-// stage of every integrator (RK3 9.11 -> 8.92 ms, RK4 10.74 -> 9.16, RK6
-// 16.06 -> 13.97); the generic body stays faster for the intermediate RK6
-// stages with 2..5 terms (8.97 vs 9.17 ms at two terms, 14.4 vs 26.1 at five).
+// Stage signatures (kSigs index) that take the 3D order-4 tensor-core body:
+// all of them since the per-signature register caps (stage_minb) let the
+// many-term RK6 stages keep their face loads in flight (C4, 128^3: the 2..5
+// term stages 6.75 / 7.55 / 8.24 / 9.31 ms vs 8.51 / 9.14 / 9.87 / 11.53 ms in
+// the generic body).
 #ifndef NDGX_MMA3_SIGS
-#define NDGX_MMA3_SIGS 0x10F
+#define NDGX_MMA3_SIGS 0x1FF
 #endif
 
 template <int DIM, int N, int KIND>
@@ -453,57 +453,77 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
   // ---------------------------------------------------------- volume on the tensor cores
   double* acc = sF;  // F_x's slots become the running dudt
   const bool krow = r < N;
+  const int rr = r & 3;  // rows 4-7 of the MMA are zero rows: their lanes mirror rows 0-3 (results unused)
 #pragma unroll
-  for (int d = 0; d < DIM; ++d) {
+  for (int d = 0; d < DIM - 1; ++d) {
     if (d > 0) __syncwarp();  // the previous axis' partial sums are stored
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
-        const int o0 = G::node(d, 8 * g + 2 * c, r), o1 = G::node(d, 8 * g + 2 * c + 1, r);
-        const int q0 = sw(0, o0), q1 = sw(0, o1);  // their accumulator slots
+        const int q0 = sw(0, G::node(d, 8 * g + 2 * c, rr)), q1 = sw(0, G::node(d, 8 * g + 2 * c + 1, rr));
         double c0 = 0.0, c1 = 0.0;
-        if (d > 0 && krow) {
+        if (d > 0) {
           c0 = acc[v * NPE + q0];
           c1 = acc[v * NPE + q1];
         }
         const double b = sF[(d * NV + v) * NPE + sw(d, G::node(d, 8 * g + r, c))];
         dmma_8x8x4(ln.k[d], b, c0, c1);
-        if (d < DIM - 1) {
-          __syncwarp();  // B/C reads of this group precede the in-place stores
-          if (krow) {
-            acc[v * NPE + q0] = c0;
-            acc[v * NPE + q1] = c1;
-          }
-        } else if (krow) {
-          // final axis: outputs at nodes o0, o0 + 1 = line + 16 r; lifted faces
-          double dv[2] = {c0, c1};
-#pragma unroll
-          for (int s2 = 0; s2 < 2; ++s2) {
-            const int n = s2 ? o1 : o0;
-            const int i = n & 3, j = (n >> 2) & 3, kk = n >> 4;
-            constexpr int X0 = 0, Y0 = 2, Z0 = 4;
-            const int xl = X0 + (RA == 0 ? par : 0), zl = Z0 + (RA == 2 ? par : 0);  // run-axis slots alternate
-            if (i == 0) dv[s2] = fma(p.lift[0], sH[(xl * NV + v) * L + j + 4 * kk], dv[s2]);
-            if (i == N - 1) dv[s2] = fma(-p.lift[0], sH[((2 * X0 + 1 - xl) * NV + v) * L + j + 4 * kk], dv[s2]);
-            if (j == 0) dv[s2] = fma(p.lift[1], sH[(Y0 * NV + v) * L + i + 4 * kk], dv[s2]);
-            if (j == N - 1) dv[s2] = fma(-p.lift[1], sH[((Y0 + 1) * NV + v) * L + i + 4 * kk], dv[s2]);
-            if (kk == 0) dv[s2] = fma(p.lift[2], sH[(zl * NV + v) * L + i + 4 * j], dv[s2]);
-            if (kk == N - 1) dv[s2] = fma(-p.lift[2], sH[((2 * Z0 + 1 - zl) * NV + v) * L + i + 4 * j], dv[s2]);
-          }
-          const double k0 = dv[0] * dt, k1 = dv[1] * dt;
-          double* gout = p.out + ebase + v * NPE + o0;  // o1 == o0 + 1
-          if (!LAST) {
-            *reinterpret_cast<double2*>(gout) = make_double2(k0, k1);
-          } else {
-            const double u0 = fma(p.b_last, k0, sS[v * NPE + q0]);
-            const double u1 = fma(p.b_last, k1, sS[v * NPE + q1]);
-            *reinterpret_cast<double2*>(gout) = make_double2(u0, u1);
-            acc[v * NPE + q0] = u0;  // u_new for the finite check / next alpha
-            acc[v * NPE + q1] = u1;
-          }
+        __syncwarp();  // B/C reads of this group precede the in-place stores
+        if (krow) {
+          acc[v * NPE + q0] = c0;
+          acc[v * NPE + q1] = c1;
         }
       }
+    }
+  }
+  __syncwarp();
+  // final axis (z): outputs of line group g at nodes o0 = 8g + 2c + 16 rr and
+  // o0 + 1; the g = 1 results move to lanes 16-31, so every lane finishes one
+  // output pair per variable (lifted faces and the RK epilogue, branch-free)
+  const int gl = lane >> 4;                       // this lane's line group
+  const int o0 = 8 * gl + 2 * c + 16 * rr;
+  const int qa = sw(0, o0), qb = sw(0, o0 + 1);
+  const int jj = 2 * gl + (c >> 1), i0 = (2 * c) & 3;
+  constexpr int X0 = 0, Y0 = 2, Z0 = 4;
+  const int xl = X0 + (RA == 0 ? par : 0), zl = Z0 + (RA == 2 ? par : 0);  // run-axis slots alternate
+  // face-lift coefficients of the two outputs (0 off the face)
+  const double xc0 = (c & 1) == 0 ? p.lift[0] : 0.0, xc1 = (c & 1) != 0 ? -p.lift[0] : 0.0;
+  const double yc = gl == 0 ? (c < 2 ? p.lift[1] : 0.0) : (c >= 2 ? -p.lift[1] : 0.0);
+  const double zc = rr == 0 ? p.lift[2] : (rr == N - 1 ? -p.lift[2] : 0.0);
+  const double* hx0 = sH + xl * NV * L + jj + 4 * rr;
+  const double* hx1 = sH + (2 * X0 + 1 - xl) * NV * L + jj + 4 * rr;
+  const double* hy = sH + (Y0 + gl) * NV * L + i0 + 4 * rr;
+  const double* hz = sH + (rr == 0 ? zl : 2 * Z0 + 1 - zl) * NV * L + i0 + 4 * jj;
+  double* gout = p.out + ebase + o0;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double c0[2], c1[2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      c0[g] = acc[v * NPE + sw(0, G::node(2, 8 * g + 2 * c, rr))];
+      c1[g] = acc[v * NPE + sw(0, G::node(2, 8 * g + 2 * c + 1, rr))];
+      const double b = sF[(2 * NV + v) * NPE + sw(2, G::node(2, 8 * g + r, c))];
+      dmma_8x8x4(ln.k[2], b, c0[g], c1[g]);
+    }
+    const double y0 = __shfl_sync(0xffffffffu, c0[1], lane & 15), y1 = __shfl_sync(0xffffffffu, c1[1], lane & 15);
+    double d0 = gl ? y0 : c0[0], d1 = gl ? y1 : c1[0];
+    d0 = fma(xc0, hx0[v * L], d0);
+    d1 = fma(xc1, hx1[v * L], d1);
+    d0 = fma(yc, hy[v * L], d0);
+    d1 = fma(yc, hy[v * L + 1], d1);
+    d0 = fma(zc, hz[v * L], d0);
+    d1 = fma(zc, hz[v * L + 1], d1);
+    const double k0 = d0 * dt, k1 = d1 * dt;
+    if (!LAST) {
+      *reinterpret_cast<double2*>(gout + v * NPE) = make_double2(k0, k1);
+    } else {
+      __syncwarp();  // every lane's accumulator reads of v precede the u_new stores
+      const double u0 = fma(p.b_last, k0, sS[v * NPE + qa]);
+      const double u1 = fma(p.b_last, k1, sS[v * NPE + qb]);
+      *reinterpret_cast<double2*>(gout + v * NPE) = make_double2(u0, u1);
+      acc[v * NPE + qa] = u0;  // u_new for the finite check / next alpha
+      acc[v * NPE + qb] = u1;
     }
   }
   if (LAST) {
@@ -797,15 +817,30 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
 }
 
 // ============================================================ stage kernel
+// Resident CTAs per SM the register allocation is capped for (4 warps each):
+// 4 (<= 128 registers, 16 warps) by default -- capping at 80 for 24 warps
+// measured 25% slower on the flagship (less load-level parallelism per warp).
+// The 3D order-4 Euler tensor-core body (C4) is measured per signature: the
+// u-only stage 5 (4.42 vs 4.55 ms), the one-term and the 2..5-term RK6 stages
+// 3 (<= 168 registers: a face node's loads of every K_j stay in flight;
+// 5.70-9.31 vs 6.02-20.7 ms), the last stage 4 (11.55 vs 12.79 ms).
+__host__ __device__ constexpr int stage_minb(int dim, int n, int kind, bool exact, int sig) {
+#ifdef NDGX_MINB
+  return NDGX_MINB + 0 * (dim + n + kind + (exact ? 1 : 0) + sig);
+#else
+#ifndef NDGX_MINB3
+#define NDGX_MINB3 0x435  // per signature class, hex digits: last stage | many-term | u-only
+#endif
+  return (dim == 3 && n == 4 && kind == 1 && !exact)
+             ? (sig == 0 ? (NDGX_MINB3 & 15) : (sig == 8 ? (NDGX_MINB3 >> 8 & 15) : (NDGX_MINB3 >> 4 & 15)))
+             : 4;
+#endif
+}
+
 // SIG indexes kSigs: the stage's term structure (p.nu, p.amask, p.bmask) at
 // compile time, so the term loops resolve without predicates
 template <int DIM, int N, int KIND, bool EXACT, int SIG, bool XF = false>
-// <= 128 registers (4 CTAs = 16 warps per SM): capping at 80 for 24 warps
-// measured 25% slower (less load-level parallelism per warp)
-#ifndef NDGX_MINB
-#define NDGX_MINB 4
-#endif
-__global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS, NDGX_MINB)
+__global__ void __launch_bounds__(Geo<DIM, N, KIND>::THREADS, stage_minb(DIM, N, KIND, EXACT, SIG))
 stage_kernel(const __grid_constant__ StageArgs p) {
   using G = Geo<DIM, N, KIND>;
   using A = Ar<EXACT>;
