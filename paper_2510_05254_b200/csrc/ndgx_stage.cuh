@@ -831,8 +831,14 @@ __host__ __device__ constexpr int stage_minb(int dim, int n, int kind, bool exac
 #ifndef NDGX_MINB3
 #define NDGX_MINB3 0x435  // per signature class, hex digits: last stage | many-term | u-only
 #endif
+#ifndef NDGX_MINB2
+#define NDGX_MINB2 0x444  // the 2D order-8 Euler flagship, same classes: last (bm != 0) | others | u-only
+#endif
   return (dim == 3 && n == 4 && kind == 1 && !exact)
              ? (sig == 0 ? (NDGX_MINB3 & 15) : (sig == 8 ? (NDGX_MINB3 >> 8 & 15) : (NDGX_MINB3 >> 4 & 15)))
+         : (dim == 2 && n == 8 && kind == 1 && !exact)
+             ? (sig == 0 ? (NDGX_MINB2 & 15)
+                         : ((kSigs[sig].bm != 0) ? (NDGX_MINB2 >> 8 & 15) : (NDGX_MINB2 >> 4 & 15)))
              : 4;
 #endif
 }
