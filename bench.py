@@ -319,12 +319,27 @@ def bench_ours(args):
     # pinned host state (the reference AoS layout), synthetic IC of this block
     host = torch.empty(dof, dtype=torch.float64, pin_memory=True)
     u0 = host.numpy()
+    t0 = time.perf_counter()
     if ranked:
         ndgx.init_block(cfg, lo, hi, out=u0)
     elif eq:
         ndgx.init_euler_subsonic(mesh, model, out=u0)
     else:
         ndgx.init_multisine(mesh, model, n_modes=40, seed=42, out=u0)
+    t_host_init = time.perf_counter() - t0
+    # the same IC generated in HBM (f4: ndgx_init_device), timed for the setup
+    # comparison; the uploads below overwrite it with the host field
+    ic_amps = None if eq else ndgx.multisine_amplitudes(40, 42)
+    s.init_device(ndgx.IC_EULER_SUBSONIC if eq else ndgx.IC_MULTISINE, ic_amps)  # first call: module load
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    s.init_device(ndgx.IC_EULER_SUBSONIC if eq else ndgx.IC_MULTISINE, ic_amps)
+    torch.cuda.synchronize(dev)
+    t_dev_init = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    s.upload_ptr(host.data_ptr())
+    torch.cuda.synchronize(dev)
+    t_upload = time.perf_counter() - t0
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -497,6 +512,9 @@ def bench_ours(args):
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * dof / args.steps,
                     "d2h_bytes_per_step": 8 * dof / args.steps,
                     "note": "one advance(StepPlan{K}) call: pinned host AoS upload, K steps, download"},
+            "setup": {"host_init_s": t_host_init, "upload_s": t_upload, "device_init_s": t_dev_init,
+                      "note": "initial condition of this rank's block: host init_* + pinned H2D upload "
+                              "vs ndgx_init_device (generated in HBM, no host field)"},
             "exact_mode": exact,
             "scale_rows": scale_rows,
             "gpu_launches": launches,

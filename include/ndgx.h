@@ -217,6 +217,28 @@ int ndgx_get_block(const ndgx_solver* s, int worker, ndgx_rank_plan* plan); /* B
 int ndgx_dump_field(ndgx_solver* s, const char* path, ndgx_error* err);
 int ndgx_load_field(ndgx_solver* s, const char* path, ndgx_error* err);
 
+/* Initial conditions and diagnostics on the device,
+ * over the handle's current state in HBM (every block of the handle; a rank
+ * solver's own block):
+ *   ndgx_init_device              <- init_multisine (src/grid.cpp:135-156, ic
+ *                                    NDGX_IC_MULTISINE with the amplitudes of
+ *                                    multisine_amplitudes, :127-133) /
+ *                                    init_euler_subsonic (:162-188) + upload,
+ *                                    without a host field or an H2D copy
+ *   ndgx_conserved_totals_device  <- conserved_totals (src/grid.cpp:205-213), out[nvar]
+ *   ndgx_l2_error_ic_device       <- l2_error(state, init_*(...), var) (src/grid.cpp:190-203),
+ *                                    the IC evaluated on the fly (experiments.cpp:112, 508)
+ *   ndgx_l1_norm_device           <- l1_norm (src/grid.cpp:215-223)
+ * Same ConfigError messages as the reference.  Values follow the reference's
+ * expressions (explicit roundings); device sin and the tree-ordered sums make
+ * them equal to the host functions to ~1e-16 / ~1e-15 relative. */
+typedef enum { NDGX_IC_MULTISINE = 0, NDGX_IC_EULER_SUBSONIC = 1 } ndgx_ic;
+int ndgx_init_device(ndgx_solver* s, int ic, const double* amplitudes, int n_modes, ndgx_error* err);
+int ndgx_conserved_totals_device(ndgx_solver* s, double* out, ndgx_error* err);
+int ndgx_l2_error_ic_device(ndgx_solver* s, int ic, const double* amplitudes, int n_modes, int var, double* out,
+                            ndgx_error* err);
+int ndgx_l1_norm_device(ndgx_solver* s, int var, double* out, ndgx_error* err);
+
 /* Library identification: "ndgx <version> sm_100a". */
 const char* ndgx_version(void);
 

@@ -4,7 +4,7 @@ The compute path is libndgx.so (hand-written sm_100a CUDA behind the C ABI in
 include/ndgx.h); ``ndgx`` mirrors the reference solver's API on top of it.
 """
 from . import report  # noqa: F401
-from .ndgx import (ADVECTION, ARITH_EXACT, ARITH_FAST, EULER_ISOTHERMAL, RK3, RK4, RK6,  # noqa: F401
+from .ndgx import (ADVECTION, ARITH_EXACT, ARITH_FAST, EULER_ISOTHERMAL, IC_EULER_SUBSONIC, IC_MULTISINE, RK3, RK4, RK6,  # noqa: F401
                    AdvanceResult, Block, BlockDecomposition, ConfigError, CudaError,
                    DecompositionError, EquationModel, InstabilityError, Mesh, NdgError,
                    PhysicsError, RunError, Solver, SolverConfig, StepPlan, StepStats,

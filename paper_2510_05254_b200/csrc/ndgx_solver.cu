@@ -39,6 +39,7 @@
 #include <vector>
 
 #include "ndgx.h"
+#include "ndgx_field.cuh"
 #include "ndgx_kernels.h"
 #include "ndgx_nccl.h"
 #include "ndgx_setup.h"
@@ -222,6 +223,7 @@ struct ndgx_solver {
   int64_t hdof = 0;
   bool exact = true;
   double K[3][64]{}, lift[3]{}, a[7][7]{}, b[7]{};
+  double gl_nodes[8]{}, gl_weights[8]{};  // the quadrature rule (device ICs and diagnostics)
   double cflh = 0.0, two_n_minus_1 = 0.0, const_alpha = -1.0;
   ndgx::StageKernel kern;
   ndgx::StageLaunch lcfg[ndgx::kNumSigs];  // per stage signature (ndgx::kSigs)
@@ -965,6 +967,8 @@ static int create_blocks(const ndgx_problem* prob, const std::vector<ndgx_rank_p
       ndgx_differentiation_matrix(s->N, nodes, diff);
     }
     ndgx::build_operator(&s->p, nodes, weights, diff, s->K, s->lift);
+    std::memcpy(s->gl_nodes, nodes, sizeof(double) * s->N);
+    std::memcpy(s->gl_weights, weights, sizeof(double) * s->N);
     ndgx::rk_tableau(prob->rk, &s->stages, s->a, s->b);
     s->cflh = ndgx::dt_numerator(&s->p);
     s->two_n_minus_1 = (double)(2 * s->N - 1);
@@ -1184,6 +1188,183 @@ static std::string fmt_len(double v) {  // std::ostream << double (precision 6, 
   o << v;
   return o.str();
 }
+
+// ------------------------------------------------------------ f4: device ICs and diagnostics
+static ndgx::FieldArgs field_args(const ndgx_solver* s, const Blk& bk) {
+  ndgx::FieldArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.u = ndgx_solver::u_buf(bk, s->parity);
+  a.dim = s->dim;
+  a.N = s->N;
+  a.nv = s->nv;
+  a.npe = s->npe;
+  a.jac = 1.0;
+  for (int d = 0; d < 3; ++d) {
+    a.cells[d] = bk.cells[d];
+    a.goff[d] = bk.goff[d];
+    a.dx[d] = s->p.length[d] / s->gcells[d];  // Mesh::cell_size (grid.hpp:27)
+    if (d < s->dim) a.jac *= 0.5 * a.dx[d];   // src/grid.cpp:33-34
+  }
+  for (int q = 0; q < s->N; ++q) {
+    a.nodes[q] = s->gl_nodes[q];
+    a.weights[q] = s->gl_weights[q];
+  }
+  a.sound_speed = s->p.sound_speed;
+  a.ic = -1;
+  return a;
+}
+
+// the reference's init_* ConfigErrors (src/grid.cpp:135-170)
+static int check_ic(const ndgx_solver* s, int ic, const double* amps, int n_modes, ndgx_error* err) {
+  if (ic == NDGX_IC_MULTISINE) {
+    if (s->kind != NDGX_ADVECTION) {
+      set_error(err, NDGX_ERR_CONFIG, "init_multisine applies to the advection scalar only");
+      return NDGX_ERR_CONFIG;
+    }
+    if (n_modes < 1 || !amps) {
+      set_error(err, NDGX_ERR_CONFIG, "multisine: need at least one mode");
+      return NDGX_ERR_CONFIG;
+    }
+    if (n_modes > ndgx::kMaxModes) {
+      set_error(err, NDGX_ERR_CONFIG, "multisine: more than 256 modes on the device path");
+      return NDGX_ERR_CONFIG;
+    }
+  } else if (ic == NDGX_IC_EULER_SUBSONIC) {
+    if (s->kind != NDGX_EULER_ISOTHERMAL) {
+      set_error(err, NDGX_ERR_CONFIG, "init_euler_subsonic requires an isothermal Euler model");
+      return NDGX_ERR_CONFIG;
+    }
+    if (s->dim < 2) {
+      set_error(err, NDGX_ERR_CONFIG, "init_euler_subsonic is defined for 2D/3D meshes");
+      return NDGX_ERR_CONFIG;
+    }
+  } else {
+    set_error(err, NDGX_ERR_CONFIG, "unknown initial condition");
+    return NDGX_ERR_CONFIG;
+  }
+  return NDGX_OK;
+}
+
+// the amplitudes on the block's device (freed by the caller)
+static double* device_amps(const double* amps, int n_modes) {
+  if (!amps || n_modes <= 0) return nullptr;
+  double* d = nullptr;
+  ck(cudaMalloc(&d, sizeof(double) * n_modes), "cudaMalloc amplitudes");
+  ck(cudaMemcpy(d, amps, sizeof(double) * n_modes, cudaMemcpyHostToDevice), "copy amplitudes");
+  return d;
+}
+
+static unsigned field_grid(const Blk& bk, int npe) {
+  const long long nodes = (long long)bk.cells[0] * bk.cells[1] * bk.cells[2] * npe;
+  return (unsigned)std::max<long long>(1, std::min<long long>((nodes + 255) / 256, 148LL * 8));
+}
+
+// Weighted sums of the handle's blocks (what: 0 totals, 1 l2 vs the IC, 2
+// l1), CTA partials summed in index order, blocks in worker order.
+static void device_sums(ndgx_solver* s, int what, int var, int ic, const double* amps, int n_modes, double* out) {
+  const int nout = what == 0 ? s->nv : 1;
+  for (int k = 0; k < nout; ++k) out[k] = 0.0;
+  for (const Blk& bk : s->blk) {
+    s->on(bk);
+    ndgx::FieldArgs a = field_args(s, bk);
+    a.what = what;
+    a.var = var;
+    a.ic = ic;
+    a.n_modes = n_modes;
+    double* damps = device_amps(amps, n_modes);
+    a.amps = damps;
+    const unsigned grid = field_grid(bk, s->npe);
+    double* part = nullptr;
+    ck(cudaMalloc(&part, sizeof(double) * grid * nout), "cudaMalloc partials");
+    ndgx::diag_kernel<<<grid, 256, 0, bk.st>>>(a, part);
+    ck(cudaGetLastError(), "diag launch");
+    std::vector<double> h((size_t)grid * nout);
+    ck(cudaMemcpyAsync(h.data(), part, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, bk.st), "partials");
+    ck(cudaStreamSynchronize(bk.st), "diag sync");
+    cudaFree(part);
+    if (damps) cudaFree(damps);
+    for (unsigned q = 0; q < grid; ++q)
+      for (int k = 0; k < nout; ++k) out[k] += h[(size_t)q * nout + k];
+  }
+  s->on(s->blk[0]);
+}
+
+extern "C" {
+
+int ndgx_init_device(ndgx_solver* s, int ic, const double* amplitudes, int n_modes, ndgx_error* err) {
+  clear_error(err);
+  if (!s) return NDGX_ERR_CONFIG;
+  if (int rc = check_ic(s, ic, amplitudes, n_modes, err)) return rc;
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    for (const Blk& bk : s->blk) {
+      s->on(bk);
+      ndgx::FieldArgs a = field_args(s, bk);
+      a.ic = ic;
+      a.n_modes = ic == NDGX_IC_MULTISINE ? n_modes : 0;
+      double* damps = device_amps(ic == NDGX_IC_MULTISINE ? amplitudes : nullptr, a.n_modes);
+      a.amps = damps;
+      ndgx::init_field_kernel<<<field_grid(bk, s->npe), 256, 0, bk.st>>>(a);
+      ck(cudaGetLastError(), "init launch");
+      ck(cudaStreamSynchronize(bk.st), "init sync");
+      if (damps) cudaFree(damps);
+    }
+    s->on(s->blk[0]);
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+  return NDGX_OK;
+}
+
+int ndgx_conserved_totals_device(ndgx_solver* s, double* out, ndgx_error* err) {
+  clear_error(err);
+  if (!s || !out) return NDGX_ERR_CONFIG;
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    device_sums(s, 0, 0, -1, nullptr, 0, out);
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+  return NDGX_OK;
+}
+
+int ndgx_l2_error_ic_device(ndgx_solver* s, int ic, const double* amplitudes, int n_modes, int var, double* out,
+                            ndgx_error* err) {
+  clear_error(err);
+  if (!s || !out) return NDGX_ERR_CONFIG;
+  if (int rc = check_ic(s, ic, amplitudes, n_modes, err)) return rc;
+  if (var < 0 || var >= s->nv) {
+    set_error(err, NDGX_ERR_CONFIG, "l2_error: bad variable");
+    return NDGX_ERR_CONFIG;
+  }
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    device_sums(s, 1, var, ic, ic == NDGX_IC_MULTISINE ? amplitudes : nullptr,
+                ic == NDGX_IC_MULTISINE ? n_modes : 0, out);
+    *out = std::sqrt(*out);
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+  return NDGX_OK;
+}
+
+int ndgx_l1_norm_device(ndgx_solver* s, int var, double* out, ndgx_error* err) {
+  clear_error(err);
+  if (!s || !out) return NDGX_ERR_CONFIG;
+  if (var < 0 || var >= s->nv) {
+    set_error(err, NDGX_ERR_CONFIG, "l1_norm: bad variable");
+    return NDGX_ERR_CONFIG;
+  }
+  try {
+    ck(cudaSetDevice(s->p.device), "cudaSetDevice");
+    device_sums(s, 2, var, -1, nullptr, 0, out);
+  } catch (const CudaFailure& f) {
+    return cuda_error(err, f);
+  }
+  return NDGX_OK;
+}
+
+}  // extern "C"
 
 int ndgx_dump_field(ndgx_solver* s, const char* path, ndgx_error* err) {
   clear_error(err);

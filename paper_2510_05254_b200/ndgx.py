@@ -34,6 +34,7 @@ RK3, RK4, RK6 = 0, 1, 2
 RK_NAMES = {"rk3": RK3, "rk4": RK4, "rk6": RK6}
 RK_STAGES = {RK3: 3, RK4: 4, RK6: 7}
 ARITH_EXACT, ARITH_FAST = 0, 1
+IC_MULTISINE, IC_EULER_SUBSONIC = 0, 1  # ndgx_ic: device initial conditions
 
 
 # ----------------------------------------------------------------- errors
@@ -156,6 +157,10 @@ def lib() -> C.CDLL:
     L.ndgx_load_field.argtypes = [C.c_void_p, C.c_char_p, P(Error)]
     L.ndgx_init_multisine_block.argtypes = [P(Problem), D, C.c_int, P(C.c_int), P(C.c_int), D]
     L.ndgx_init_euler_subsonic_block.argtypes = [P(Problem), P(C.c_int), P(C.c_int), D]
+    L.ndgx_init_device.argtypes = [C.c_void_p, C.c_int, D, C.c_int, P(Error)]
+    L.ndgx_conserved_totals_device.argtypes = [C.c_void_p, D, P(Error)]
+    L.ndgx_l2_error_ic_device.argtypes = [C.c_void_p, C.c_int, D, C.c_int, C.c_int, D, P(Error)]
+    L.ndgx_l1_norm_device.argtypes = [C.c_void_p, C.c_int, D, P(Error)]
     _lib = L
     return L
 
@@ -463,6 +468,41 @@ class Solver:
         """Restart from an ndgfield dump (load_field, src/field_io.cpp:36-72)."""
         err = Error()
         _check(lib().ndgx_load_field(self._h, os.fsencode(path), C.byref(err)), err)
+
+    # ------------------------------------------------ f4: device ICs and diagnostics
+    def init_device(self, ic: int, amplitudes=None) -> None:
+        """Generate the initial condition straight into HBM (init_multisine /
+        init_euler_subsonic, src/grid.cpp:135-188, + upload): no host field,
+        no H2D copy.  `amplitudes` (multisine) as from multisine_amplitudes."""
+        amps = None if amplitudes is None else np.ascontiguousarray(amplitudes, dtype=np.float64)
+        err = Error()
+        _check(lib().ndgx_init_device(self._h, ic, None if amps is None else _dptr(amps),
+                                      0 if amps is None else len(amps), C.byref(err)), err)
+
+    def conserved_totals_device(self) -> np.ndarray:
+        """conserved_totals of the device state (src/grid.cpp:205-213)."""
+        out = np.zeros(4)
+        err = Error()
+        _check(lib().ndgx_conserved_totals_device(self._h, _dptr(out), C.byref(err)), err)
+        return out[:self.config.model.n_var()].copy()
+
+    def l2_error_ic_device(self, ic: int, amplitudes=None, var: int = 0) -> float:
+        """l2_error(state, init_*(...), var) with the IC evaluated on the fly
+        (src/grid.cpp:190-203; the experiments' error, src/experiments.cpp:112)."""
+        amps = None if amplitudes is None else np.ascontiguousarray(amplitudes, dtype=np.float64)
+        out = np.zeros(1)
+        err = Error()
+        _check(lib().ndgx_l2_error_ic_device(self._h, ic, None if amps is None else _dptr(amps),
+                                             0 if amps is None else len(amps), var, _dptr(out),
+                                             C.byref(err)), err)
+        return float(out[0])
+
+    def l1_norm_device(self, var: int = 0) -> float:
+        """l1_norm of the device state (src/grid.cpp:215-223)."""
+        out = np.zeros(1)
+        err = Error()
+        _check(lib().ndgx_l1_norm_device(self._h, var, _dptr(out), C.byref(err)), err)
+        return float(out[0])
 
     @property
     def stream(self) -> int:
