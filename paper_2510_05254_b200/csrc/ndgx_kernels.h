@@ -13,7 +13,7 @@ struct StageKernel {
   StageFn fn[kNumSigs] = {};  // by stage signature (kSigs)
   StageFn fnx[kNumSigs] = {}; // region-3 (x-filtered interior) launches: the x-run variant where one exists
   int threads = 0;
-  int warps = 0;            // elements in flight per CTA (one per warp)
+  int warps = 0;            // elements in flight per CTA (EPW per warp)
   int smem_fixed[kNumSigs] = {};  // dynamic shared memory without the element rings, per signature
   int ring_per_array = 0;   // ring bytes per slot per input array (all warps of a CTA)
   bool tma_ok = false;      // element chunks are 16-byte multiples (bulk copies)
@@ -52,7 +52,7 @@ StageKernel make_stage_kernel() {
     k.fnx[8] = &stage_kernel<DIM, N, KIND, EXACT, 8, true>;
   }
   k.threads = G::THREADS;
-  k.warps = G::WARPS;
+  k.warps = G::WARPS * G::EPW;
   for (int q = 0; q < kNumSigs; ++q)
     k.smem_fixed[q] = G::smem_bytes(0, 0, G::mma_body(EXACT, q), kSigs[q].bm != 0);
   k.ring_per_array = G::WARPS * G::SLOT1 * 8;

@@ -73,7 +73,23 @@ struct Geo {
   static constexpr int RED = 2 * WARPS;                      // block reduction scratch (doubles)
   static constexpr int HEAD = WARPS * MAXD + RED;            // 8-byte words before the slabs
   static constexpr int CHUNK = NV * NPE;                     // one array of one element (doubles)
-  static constexpr bool TMA_OK = (CHUNK % 2) == 0;           // 16-byte element chunks
+  // generic body: lanes per element (GL) and elements per warp (EPW).  Small
+  // elements share a warp so the node and face passes keep the lanes busy:
+  // 2D o4 16 lanes (1 node + 1 face node each), o5 / o6 8 lanes (4 / 5 node
+  // passes, 3 face passes), o2 / o3 4 lanes, 1D 4-8 lanes, 3D o2 8 lanes.
+  static constexpr int group_lanes() {
+    return DIM == 1 ? (N <= 4 ? 4 : 8)
+                    : (DIM == 2 ? (N <= 3 ? 4 : (N == 4 ? 16 : (N <= 6 ? 8 : 32))) : (N == 2 ? 8 : 32));
+  }
+#ifdef NDGX_GL
+  static constexpr int GL = NDGX_GL < group_lanes() ? group_lanes() : NDGX_GL;  // tuning: fewer groups
+#else
+  static constexpr int GL = group_lanes();
+#endif
+  static constexpr int EPW = 32 / GL;
+  static constexpr int NMG = (NPE + GL - 1) / GL;            // node passes of a lane
+  static constexpr int FMG = (FN + GL - 1) / GL;             // face passes of a lane
+  static constexpr bool TMA_OK = (CHUNK % 2) == 0 && GL == 32;  // 16-byte element chunks, one element per warp
   static constexpr bool MMA = (DIM == 2 && N == 8);          // FAST-mode tensor-core volume (2D)
   static constexpr bool MMA3 = (DIM == 3 && N == 4);         // FAST-mode tensor-core volume (3D)
   // one face node per lane: the ring slot also carries the element's face
@@ -86,7 +102,7 @@ struct Geo {
   static constexpr __host__ __device__ int wslab(bool mma, bool last) {
     return mma ? (MMA3 ? (((3 + (last ? 1 : 0)) * NV * NPE + FACES * (NV + 1) * L + FACES * NV * L + 1) & ~1)
                        : (((1 + (last ? 1 : 0)) * NV * NPE + FACES * HW * L + FACES * NV * L + 1) & ~1))
-               : WSLAB;
+               : EPW * WSLAB;
   }
   // which body a (arith, signature) kernel runs: the 2D N=8 / 3D N=4
   // tensor-core bodies (contracted mode; 3D for the NDGX_MMA3_SIGS stages)
@@ -1048,171 +1064,181 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       e = nelem;  // done: skip the element loop below
     }
   }
-  // the generic body (exact mode, and the contracted shapes without a tensor-core body)
+  // The generic body (exact mode, and the contracted shapes without a
+  // tensor-core body).  Small elements are processed G::GL lanes per element,
+  // G::EPW elements per warp (lane group `grp`, lane `sub` in the group):
+  // every lane of a group runs the one-element code with `sub` for `lane`
+  // and GL for 32, on its own slab.  `act` false: the lane only keeps the
+  // warp's barriers (no element, or one the launch's region skips).
   auto generic_element = [&](const int e, const int cx, const int cy, const int cz, const double* src,
-                             const double* fsrc) {
+                             const double* fsrc, const bool act) {
+    constexpr int GL = G::GL;
+    const int sub = GL == 32 ? lane : (lane & (GL - 1)), grp = GL == 32 ? 0 : lane / GL;
+    double* const gF = sF + grp * G::WSLAB;
+    double* const gT = gF + G::OFF_T;
+    double* const gH = gF + G::OFF_H;
     const size_t ebase = (size_t)e * NV * NPE;
-      auto aos_cell = [&]() -> long long {  // global AoS cell index of this element
-        const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
-        return (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz;
-      };
+    auto aos_cell = [&]() -> long long {  // global AoS cell index of this element
+      const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
+      return (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz;
+    };
 
-      // ------------------------------------------------ 1: nodes
-      // lane's nodes: n = lane + 32m
-      double Sn[G::NM][NV];  // last stage: S at the lane's nodes
-  #pragma unroll
-      for (int m = 0; m < G::NM; ++m) {
-        const int n = lane + 32 * m;
-        if (n >= NPE) continue;
-        double U[NV];
-  #pragma unroll
+    // ------------------------------------------------ 1: nodes
+    // lane's nodes: n = sub + GL m
+    double Sn[G::NMG][NV];  // last stage: S at the lane's nodes
+#pragma unroll
+    for (int m = 0; m < G::NMG; ++m) {
+      const int n = sub + GL * m;
+      if (!act || n >= NPE) continue;
+      double U[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double S;
+        if (depth > 0)
+          combine_s<EXACT, NU, AM, BM>(p, src + v * NPE + n, G::CHUNK, last, U[v], S);
+        else
+          combine_g<EXACT, NU, AM, BM>(p, ebase + (size_t)v * NPE + n, last, U[v], S);
+        Sn[m][v] = S;
+      }
+      if (KIND == 1 && !(U[0] > 0.0)) {
+        // first bad node of the reference's x-volume traversal: (cell, (j,k), i)
+        const int i = n % N, j = (n / N) % N, k = n / (N * N);
+        const int nkey = (DIM == 2) ? j * N + i : (j * N + k) * N + i;
+        record_error(ctl, error_key(step, p.phase, aos_cell(), nkey));
+      }
+      const double rinv = (!EXACT && KIND == 1) ? fast_rcp(U[0]) : -1.0;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double F[NV], sp;
+        flux<DIM, KIND, EXACT>(p, U, d, F, sp, rinv);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) gF[(d * NV + v) * NPE + n] = F[v];
+        const int k = G::pos_of(d, n);
+        if (k == 0 || k == N - 1) {
+          double* t = gT + ((2 * d + (k == 0 ? 0 : 1)) * HW) * L + G::line_of(d, n);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            t[v * L] = U[v];
+            if (!GEN_UTRACE) t[(NV + v) * L] = F[v];
+          }
+          if (!GEN_UTRACE) t[2 * NV * L] = sp;
+        }
+      }
+    }
+    __syncwarp();
+
+    // ------------------------------------------------ 2: face fluxes
+#pragma unroll
+    for (int m = 0; m < G::FMG; ++m) {
+      const int q = sub + GL * m;
+      if (!act || q >= G::FN) continue;
+      const int f = q / L, t = q - f * L;
+      const int d = f >> 1, side = f & 1;
+      const double* own = gT + (f * HW) * L + t;
+      // neighbour across (d, side): periodic wrap in this block, or the received plane
+      const int ca = d == 0 ? cx : (d == 1 ? cy : cz);
+      const int cn = d == 0 ? C0 : (d == 1 ? C1 : C2);
+      const bool boundary = side ? (ca == cn - 1) : (ca == 0);
+      double Un[NV];
+      if (G::FACE_PF && depth > 0) {
+        const bool ext = boundary && p.ext[d][side] != nullptr;
+#pragma unroll
         for (int v = 0; v < NV; ++v) {
           double S;
-          if (depth > 0)
-            combine_s<EXACT, NU, AM, BM>(p, src + v * NPE + n, G::CHUNK, last, U[v], S);
-          else
-            combine_g<EXACT, NU, AM, BM>(p, ebase + (size_t)v * NPE + n, last, U[v], S);
-          Sn[m][v] = S;
+          if (ext) Un[v] = fsrc[v * 32 + lane];
+          else combine_s<EXACT, NU, AM, BM>(p, fsrc + v * 32 + lane, NV * 32, false, Un[v], S);
         }
-        if (KIND == 1 && !(U[0] > 0.0)) {
-          // first bad node of the reference's x-volume traversal: (cell, (j,k), i)
-          const int i = n % N, j = (n / N) % N, k = n / (N * N);
-          const int nkey = (DIM == 2) ? j * N + i : (j * N + k) * N + i;
-          record_error(ctl, error_key(step, p.phase, aos_cell(), nkey));
+      } else if (boundary && p.ext[d][side] != nullptr) {
+        const size_t xs = d == 0 ? (size_t)cy + (size_t)C1 * cz
+                                 : (d == 1 ? (size_t)cx + (size_t)C0 * cz : (size_t)cx + (size_t)C0 * cy);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) Un[v] = __ldg(p.ext[d][side] + (xs * NV + v) * L + t);
+      } else {
+        // neighbour element index: e -/+ stride_d, wrapped periodically
+        const int stride = d == 0 ? 1 : (d == 1 ? C0 : C0 * C1);
+        const int en = side ? (ca + 1 == cn ? e - (cn - 1) * stride : e + stride)
+                            : (ca == 0 ? e + (cn - 1) * stride : e - stride);
+        const size_t g = (size_t)en * (NV * NPE) + G::node(d, t, side ? 0 : N - 1);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double S;
+          combine_g<EXACT, NU, AM, BM>(p, g + (size_t)v * NPE, false, Un[v], S);
         }
-        const double rinv = (!EXACT && KIND == 1) ? fast_rcp(U[0]) : -1.0;
-  #pragma unroll
+      }
+      double Fn[NV], sn;
+      flux<DIM, KIND, EXACT>(p, Un, d, Fn, sn, (!EXACT && KIND == 1) ? fast_rcp(Un[0]) : -1.0);
+      // this element's side: U from the trace, flux and speed recomputed
+      // (the same function of the same U as in the node phase)
+      double Uo[NV], Fo[NV], so;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Uo[v] = own[v * L];
+      if (GEN_UTRACE) {
+        flux<DIM, KIND, EXACT>(p, Uo, d, Fo, so, (!EXACT && KIND == 1) ? fast_rcp(Uo[0]) : -1.0);
+      } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) Fo[v] = own[(NV + v) * L];
+        so = own[2 * NV * L];
+      }
+      const double a = dmax(side ? so : sn, side ? sn : so);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
+        const double um = side ? Uo[v] : Un[v], up = side ? Un[v] : Uo[v];
+        const double fm = side ? Fo[v] : Fn[v], fp = side ? Fn[v] : Fo[v];
+        gH[(f * NV + v) * L + t] = A::mul(0.5, A::sub(A::add(fm, fp), A::mul(a, A::sub(up, um))));
+      }
+    }
+    __syncwarp();
+
+    // ------------------------------------------------ 3: volume, faces, epilogue
+#pragma unroll
+    for (int m = 0; m < G::NMG; ++m) {
+      const int n = sub + GL * m;
+      if (!act || n >= NPE) continue;
+      double un[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double D = 0.0;
+#pragma unroll
         for (int d = 0; d < DIM; ++d) {
-          double F[NV], sp;
-          flux<DIM, KIND, EXACT>(p, U, d, F, sp, rinv);
-  #pragma unroll
-          for (int v = 0; v < NV; ++v) sF[(d * NV + v) * NPE + n] = F[v];
-          const int k = G::pos_of(d, n);
-          if (k == 0 || k == N - 1) {
-            double* t = sT + ((2 * d + (k == 0 ? 0 : 1)) * HW) * L + G::line_of(d, n);
-  #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-              t[v * L] = U[v];
-              if (!GEN_UTRACE) t[(NV + v) * L] = F[v];
-            }
-            if (!GEN_UTRACE) t[2 * NV * L] = sp;
-          }
+          const int k = G::pos_of(d, n), t = G::line_of(d, n);
+          const double* Fl = gF + (d * NV + v) * NPE;
+          const double* Kr = &p.K[d][k * N];
+          // 0 + K0 F0 + K1 F1 + ...: the leading 0 + only normalises a -0,
+          // which zero_plus (axis 0) or the add onto dudt (axes > 0) reproduces
+          double acc = A::mul(Kr[0], Fl[G::node(d, t, 0)]);
+#pragma unroll
+          for (int l = 1; l < N; ++l) acc = A::mac(acc, Kr[l], Fl[G::node(d, t, l)]);
+          D = d == 0 ? zero_plus(acc) : A::add(D, acc);
+          if (k == 0) D = A::add(D, A::mul(p.lift[d], gH[((2 * d) * NV + v) * L + t]));
+          if (k == N - 1) D = A::sub(D, A::mul(p.lift[d], gH[((2 * d + 1) * NV + v) * L + t]));
+        }
+        const size_t gi = ebase + (size_t)v * NPE + n;
+        const double kv = A::mul(D, dt);  // k_i *= dt (solver.hpp:66-67)
+        if (!last) {
+          p.out[gi] = kv;
+        } else {
+          un[v] = p.b_last != 0.0 ? A::mac(Sn[m][v], p.b_last, kv) : Sn[m][v];
+          p.out[gi] = un[v];
         }
       }
-      __syncwarp();
-
-      // ------------------------------------------------ 2: face fluxes
-  #pragma unroll
-      for (int m = 0; m < G::FM; ++m) {
-        const int q = lane + 32 * m;
-        if (q >= G::FN) continue;
-        const int f = q / L, t = q - f * L;
-        const int d = f >> 1, side = f & 1;
-        const double* own = sT + (f * HW) * L + t;
-        // neighbour across (d, side): periodic wrap in this block, or the received plane
-        const int ca = d == 0 ? cx : (d == 1 ? cy : cz);
-        const int cn = d == 0 ? C0 : (d == 1 ? C1 : C2);
-        const bool boundary = side ? (ca == cn - 1) : (ca == 0);
-        double Un[NV];
-        if (G::FACE_PF && depth > 0) {
-          const bool ext = boundary && p.ext[d][side] != nullptr;
-  #pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            double S;
-            if (ext) Un[v] = fsrc[v * 32 + lane];
-            else combine_s<EXACT, NU, AM, BM>(p, fsrc + v * 32 + lane, NV * 32, false, Un[v], S);
-          }
-        } else if (boundary && p.ext[d][side] != nullptr) {
-          const size_t xs = d == 0 ? (size_t)cy + (size_t)C1 * cz
-                                   : (d == 1 ? (size_t)cx + (size_t)C0 * cz : (size_t)cx + (size_t)C0 * cy);
-  #pragma unroll
-          for (int v = 0; v < NV; ++v) Un[v] = __ldg(p.ext[d][side] + (xs * NV + v) * L + t);
-        } else {
-          // neighbour element index: e -/+ stride_d, wrapped periodically
-          const int stride = d == 0 ? 1 : (d == 1 ? C0 : C0 * C1);
-          const int en = side ? (ca + 1 == cn ? e - (cn - 1) * stride : e + stride)
-                              : (ca == 0 ? e + (cn - 1) * stride : e - stride);
-          const size_t g = (size_t)en * (NV * NPE) + G::node(d, t, side ? 0 : N - 1);
-  #pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            double S;
-            combine_g<EXACT, NU, AM, BM>(p, g + (size_t)v * NPE, false, Un[v], S);
-          }
-        }
-        double Fn[NV], sn;
-        flux<DIM, KIND, EXACT>(p, Un, d, Fn, sn, (!EXACT && KIND == 1) ? fast_rcp(Un[0]) : -1.0);
-        // this element's side: U from the trace, flux and speed recomputed
-        // (the same function of the same U as in the node phase)
-        double Uo[NV], Fo[NV], so;
-  #pragma unroll
-        for (int v = 0; v < NV; ++v) Uo[v] = own[v * L];
-        if (GEN_UTRACE) {
-          flux<DIM, KIND, EXACT>(p, Uo, d, Fo, so, (!EXACT && KIND == 1) ? fast_rcp(Uo[0]) : -1.0);
-        } else {
-  #pragma unroll
-          for (int v = 0; v < NV; ++v) Fo[v] = own[(NV + v) * L];
-          so = own[2 * NV * L];
-        }
-        const double a = dmax(side ? so : sn, side ? sn : so);
-  #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
-          const double um = side ? Uo[v] : Un[v], up = side ? Un[v] : Uo[v];
-          const double fm = side ? Fo[v] : Fn[v], fp = side ? Fn[v] : Fo[v];
-          sH[(f * NV + v) * L + t] = A::mul(0.5, A::sub(A::add(fm, fp), A::mul(a, A::sub(up, um))));
-        }
-      }
-      __syncwarp();
-
-      // ------------------------------------------------ 3: volume, faces, epilogue
-  #pragma unroll
-      for (int m = 0; m < G::NM; ++m) {
-        const int n = lane + 32 * m;
-        if (n >= NPE) continue;
-        double un[NV];
-  #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double D = 0.0;
-  #pragma unroll
-          for (int d = 0; d < DIM; ++d) {
-            const int k = G::pos_of(d, n), t = G::line_of(d, n);
-            const double* Fl = sF + (d * NV + v) * NPE;
-            const double* Kr = &p.K[d][k * N];
-            // 0 + K0 F0 + K1 F1 + ...: the leading 0 + only normalises a -0,
-            // which zero_plus (axis 0) or the add onto dudt (axes > 0) reproduces
-            double acc = A::mul(Kr[0], Fl[G::node(d, t, 0)]);
-  #pragma unroll
-            for (int l = 1; l < N; ++l) acc = A::mac(acc, Kr[l], Fl[G::node(d, t, l)]);
-            D = d == 0 ? zero_plus(acc) : A::add(D, acc);
-            if (k == 0) D = A::add(D, A::mul(p.lift[d], sH[((2 * d) * NV + v) * L + t]));
-            if (k == N - 1) D = A::sub(D, A::mul(p.lift[d], sH[((2 * d + 1) * NV + v) * L + t]));
-          }
-          const size_t gi = ebase + (size_t)v * NPE + n;
-          const double kv = A::mul(D, dt);  // k_i *= dt (solver.hpp:66-67)
-          if (!last) {
-            p.out[gi] = kv;
+      if (last) {
+        bool fin = true;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) fin = fin && isfinite(un[v]);
+        if (!fin) record_error(ctl, error_key(step, kPhaseInstability, p.block_id, 0));
+        if (KIND == 1 && p.scan_alpha) {
+          if (!(un[0] > 0.0)) {
+            record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(), G::aos_node(n)));
           } else {
-            un[v] = p.b_last != 0.0 ? A::mac(Sn[m][v], p.b_last, kv) : Sn[m][v];
-            p.out[gi] = un[v];
-          }
-        }
-        if (last) {
-          bool fin = true;
-  #pragma unroll
-          for (int v = 0; v < NV; ++v) fin = fin && isfinite(un[v]);
-          if (!fin) record_error(ctl, error_key(step, kPhaseInstability, p.block_id, 0));
-          if (KIND == 1 && p.scan_alpha) {
-            if (!(un[0] > 0.0)) {
-              record_error(ctl, error_key(step + 1, kPhaseScan, aos_cell(), G::aos_node(n)));
-            } else {
-              double mm = 0.0;
-  #pragma unroll
-              for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[1 + d]));
-              alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[0]), p.sound_speed));
-            }
+            double mm = 0.0;
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[1 + d]));
+            alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[0]), p.sound_speed));
           }
         }
       }
+    }
     __syncwarp();  // this element's slab reads precede the next element's writes
   };
 
@@ -1235,7 +1261,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   // before it is read again (C4 stage 5: 1.5x the compulsory DRAM bytes).
   // In a z-run the z neighbours are this warp's previous and next elements,
   // and the tensor-core body takes the lo-face flux from the previous one.
-  if constexpr (DIM == 3 && NDGX_RUN3 != 0) {
+  if constexpr (DIM == 3 && NDGX_RUN3 != 0 && G::GL == 32) {
     const int plane = C0 * C1;
     if (depth == 0 && e_stride == 1 && p.region == 0 && e_lo % plane == 0 && nelem % plane == 0 && nelem > e_lo) {
       const int z0 = e_lo / plane, nz = nelem / plane - z0;
@@ -1246,7 +1272,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
           element_3d4_fast<KIND, NU, AM, BM, NDGX_RUN3 == 2 ? 2 : 0>(p, ln4, lane, ee, x, y, z, sF, sT, sH, dt, step,
                                                                     alpha, NDGX_REUSE3 != 0 && prev, par);
         else
-          generic_element(ee, x, y, z, nullptr, nullptr);
+          generic_element(ee, x, y, z, nullptr, nullptr, true);
       };
       if (NDGX_RUN3 == 2) {
         const int ZR = nz < NDGX_RUNLEN3 ? nz : NDGX_RUNLEN3;
@@ -1274,6 +1300,21 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       }
       e = nelem;  // done: skip the element loop below
     }
+  }
+
+  // generic body with several elements per warp: chunks of EPW consecutive
+  // range elements, chunk c -> warp c mod nw
+  if constexpr (G::GL < 32) {
+    const int grp = lane / G::GL;
+    const long long cnt = ((long long)nelem - e_lo + e_stride - 1) / e_stride;  // elements of this range
+    for (long long c = (long long)blockIdx.x * G::WARPS + wib; c * G::EPW < cnt; c += nw) {
+      const long long k = c * G::EPW + grp;
+      const bool have = k < cnt;
+      const int ee = (int)(e_lo + (have ? k : 0) * e_stride);
+      const int x = ee % C0, y = (ee / C0) % C1, z = ee / (C0 * C1);
+      generic_element(ee, x, y, z, nullptr, nullptr, have && !skipped(x, y, z));
+    }
+    e = nelem;  // done: skip the element loop below
   }
   for (; e < nelem; e += es) {
     const double* src = ring + slot * SLOT;  // this element's u and K_j (when depth > 0)
@@ -1319,7 +1360,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       step_coords(cx, cy, cz);
       continue;
     }
-    generic_element(e, cx, cy, cz, src, fsrc);
+    generic_element(e, cx, cy, cz, src, fsrc, true);
     if (depth > 0 && ++slot == depth) {
       slot = 0;
       parity ^= 1;
