@@ -75,14 +75,16 @@ struct Geo {
   static constexpr int CHUNK = NV * NPE;                     // one array of one element (doubles)
   // generic body: lanes per element (GL) and elements per warp (EPW).  Small
   // elements share a warp so the node and face passes keep the lanes busy:
-  // 2D o4 16 lanes (1 node + 1 face node each), o5 / o6 8 lanes (4 / 5 node
-  // passes, 3 face passes), o2 / o3 4 lanes, 1D 4-8 lanes, 3D o2 8 lanes.
+  // 2D o4 / o5 / o6 8 lanes (2 / 4 / 5 node passes, 2 / 3 / 3 face passes),
+  // 2D o6 advection and o2 / o3 4 lanes, 1D 4-8 lanes, 3D o2 8 lanes.
+  // Measured at 1e8 DOF (profiles/r02/order_sweep_*.jsonl): 2D Euler o4 16
+  // lanes 9.4e10, 8 lanes 1.03e11; 2D advection o6 8 lanes 6.5e10, 4 lanes 9.2e10.
   static constexpr int group_lanes() {
     return DIM == 1 ? (N <= 4 ? 4 : 8)
-                    : (DIM == 2 ? (N <= 3 ? 4 : (N == 4 ? 16 : (N <= 6 ? 8 : 32))) : (N == 2 ? 8 : 32));
+                    : (DIM == 2 ? (N <= 3 || (N == 6 && KIND == 0) ? 4 : (N <= 6 ? 8 : 32)) : (N == 2 ? 8 : 32));
   }
 #ifdef NDGX_GL
-  static constexpr int GL = NDGX_GL < group_lanes() ? group_lanes() : NDGX_GL;  // tuning: fewer groups
+  static constexpr int GL = NDGX_GL;  // tuning builds of one instance
 #else
   static constexpr int GL = group_lanes();
 #endif
@@ -90,8 +92,12 @@ struct Geo {
   static constexpr int NMG = (NPE + GL - 1) / GL;            // node passes of a lane
   static constexpr int FMG = (FN + GL - 1) / GL;             // face passes of a lane
   static constexpr bool TMA_OK = (CHUNK % 2) == 0 && GL == 32;  // 16-byte element chunks, one element per warp
+#ifdef NDGX_NO_MMA  // A/B builds: the contracted generic (scalar DFMA) body instead of the tensor-core bodies
+  static constexpr bool MMA = false, MMA3 = false;
+#else
   static constexpr bool MMA = (DIM == 2 && N == 8);          // FAST-mode tensor-core volume (2D)
   static constexpr bool MMA3 = (DIM == 3 && N == 4);         // FAST-mode tensor-core volume (3D)
+#endif
   // one face node per lane: the ring slot also carries the element's face
   // neighbour values ([array][var][lane], cp.async), so no load is on demand
   static constexpr bool FACE_PF = (FM == 1);
@@ -850,12 +856,15 @@ __host__ __device__ constexpr int stage_minb(int dim, int n, int kind, bool exac
 #ifndef NDGX_MINB2
 #define NDGX_MINB2 0x444  // the 2D order-8 Euler flagship, same classes: last (bm != 0) | others | u-only
 #endif
+  // (generic bodies: 2D o4 5 CTAs, 1.03e11 -> 1.05e11 Euler; 2D o6 Euler 3 CTAs, 7.2e10 -> 7.9e10)
   return (dim == 3 && n == 4 && kind == 1 && !exact)
              ? (sig == 0 ? (NDGX_MINB3 & 15) : (sig == 8 ? (NDGX_MINB3 >> 8 & 15) : (NDGX_MINB3 >> 4 & 15)))
          : (dim == 2 && n == 8 && kind == 1 && !exact)
              ? (sig == 0 ? (NDGX_MINB2 & 15)
                          : ((kSigs[sig].bm != 0) ? (NDGX_MINB2 >> 8 & 15) : (NDGX_MINB2 >> 4 & 15)))
-             : 4;
+         : (dim == 2 && n == 4 && !exact) ? 5
+         : (dim == 2 && n == 6 && kind == 1 && !exact) ? 3
+                                                        : 4;
 #endif
 }
 

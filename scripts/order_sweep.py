@@ -13,6 +13,8 @@ tag = sys.argv[1] if len(sys.argv) > 1 else "main"
 arith = ndgx.ARITH_EXACT if (len(sys.argv) > 2 and sys.argv[2] == "exact") else ndgx.ARITH_FAST
 cases = [(2, o, 1) for o in range(2, 9)] + [(2, o, 0) for o in range(2, 9)] + \
         [(1, o, 0) for o in (2, 4, 6, 8)] + [(3, o, 1) for o in (2, 3, 4, 5)] + [(3, o, 0) for o in (2, 3)]
+if len(sys.argv) > 3:  # dim:order:eq,...
+    cases = [tuple(int(x) for x in c.split(":")) for c in sys.argv[3].split(",")]
 for dim, order, eq in cases:
     target = 1.0e8
     nv = (dim + 1) if eq else 1
