@@ -12,6 +12,12 @@
 //        (block w on devices[w % devices.size()]), halos by peer stores, the
 //        reference's RunError("worker w: ...") contract
 //
+// Arithmetic: every entry takes `arith` last.  The default NDGX_ARITH_EXACT
+// is bit-identical to the reference (the reference's unfused operation
+// order: 8.1e10 DOF*stage/s on C3).  NDGX_ARITH_FAST (FMA contraction, FP64
+// tensor cores; <= 1e-12 relative L2 vs the reference) is the headline
+// throughput, 1.96e11 -- pass it explicitly.
+//
 // with the same argument meaning, return types and exceptions
 // (include/ndg/errors.hpp:13-56).  The operator coefficients are built from
 // the caller's own gauss_lobatto/differentiation_matrix, so they are bitwise
