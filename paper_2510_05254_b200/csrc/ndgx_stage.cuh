@@ -1034,7 +1034,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 #endif
   // (measured per stage: a win for the Euler last stage, 0.96 -> 0.83 ms on
   // C3, whose x-lo reuse saves two arrays' face loads; a loss elsewhere)
-  if constexpr (USE_MMA && NDGX_XRUN > 1 && KIND == 1 && LASTC) {
+#ifndef NDGX_XRUN_SIGS
+#define NDGX_XRUN_SIGS 0x109  // the u-only stage (C3 0.50 -> 0.48 ms) and the last stages (bm != 0)
+#endif
+  if constexpr (USE_MMA && NDGX_XRUN > 1 && KIND == 1 && ((NDGX_XRUN_SIGS >> SIG) & 1) != 0) {
     // (unfiltered contiguous launches, or x-filtered ones in the XF
     // instantiation: a region test inside the runs perturbs this
     // register-capped body, so the unfiltered kernel carries none)
