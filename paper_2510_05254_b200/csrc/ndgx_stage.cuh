@@ -46,6 +46,9 @@ namespace ndgx {
 // many-term RK6 stages keep their face loads in flight (C4, 128^3: the 2..5
 // term stages 6.75 / 7.55 / 8.24 / 9.31 ms vs 8.51 / 9.14 / 9.87 / 11.53 ms in
 // the generic body).
+#ifndef NDGX_LINES3
+#define NDGX_LINES3 1  // 3D order-4 contracted stages: line-task body (1) or the tensor-core body (0)
+#endif
 #ifndef NDGX_MMA3_SIGS
 #define NDGX_MMA3_SIGS 0x1FF
 #endif
@@ -106,7 +109,8 @@ struct Geo {
   // fragments); 3D stages F_x, F_y, F_z (F_x becomes the accumulator) and
   // keeps face traces of U and speed only.  Both add S at the last stage.
   static constexpr __host__ __device__ int wslab(bool mma, bool last) {
-    return mma ? (MMA3 ? (((3 + (last ? 1 : 0)) * NV * NPE + FACES * (NV + 1) * L + FACES * NV * L + 1) & ~1)
+    return mma ? (MMA3 ? (NDGX_LINES3 ? (4 + (last ? 1 : 0)) * NV * NPE  // line body: U | three dudt parts | S
+                                      : (((3 + (last ? 1 : 0)) * NV * NPE + FACES * (NV + 1) * L + FACES * NV * L + 1) & ~1))
                        : (((1 + (last ? 1 : 0)) * NV * NPE + FACES * HW * L + FACES * NV * L + 1) & ~1))
                : EPW * WSLAB;
   }
@@ -578,6 +582,250 @@ __device__ __forceinline__ void element_3d4_fast(const StageArgs& p, const Lane4
   __syncwarp();  // this element's slab reads precede the next element's writes
 }
 
+// ------------------------------------------------------------ 3D order-4 line body
+// The C4 shape (3D, N = 4, contracted) by LINE TASKS instead of tensor-core
+// tiles.  The tensor-core body moves every flux through shared memory in the
+// MMA operand layouts and carries the running dudt across the three axes
+// through shared memory: ~420 shared wavefronts per element, and the L1 pipe
+// at 95% bounds it.  Here a lane owns whole lines:
+//   1  nodes: each lane forms U_s at its node pair (16-byte loads) and stores
+//      it once into a swizzled U slab;
+//   2  lines: 48 tasks (16 lines per axis), lanes 0-15 the x lines and 16-31
+//      the y lines, then lanes 0-15 the z lines.  A task reads its line's 4
+//      nodes, computes the Lax-Friedrichs flux at the line's two ends (its
+//      face nodes: own flux = the end node's flux, neighbour from HBM / the
+//      received plane), the 4 node fluxes, D = K F (16 FMA per variable) and
+//      the lifted end fluxes, and stores the axis's dudt part;
+//   3  epilogue: each lane sums the three axis parts at its node pair.
+// About 160 shared wavefronts per element.  K_d = (dx_0 / dx_d) K_0 (exactly
+// K_0 on the equal-spacing meshes): every lane uses K_0 as constant-bank
+// operands and scales by r_d = lift_d / lift_0.  In a z-run the z lines stay
+// on lanes 0-15, so the z-lo face flux is the previous element's z-hi flux
+// carried in registers (`hc`), bitwise the value a recomputation gives.
+//
+// Slab swizzle: node n = i + 4 j + 16 k sits at n ^ (k | k << 2) (i ^= k,
+// j ^= k): every plane of fixed i, j or k maps onto 16 distinct double
+// banks, so line reads and writes along any axis are conflict-free.
+__device__ __forceinline__ int sw3(int n) {
+  const int k = n >> 4;
+  return n ^ (k | (k << 2));
+}
+
+template <int KIND, int NU, int AM, int BM>
+__device__ __forceinline__ void element_3d4_lines(const StageArgs& p, int lane, int e, int cx, int cy, int cz,
+                                                  double* sU, double* sD, double dt, long long step, double& alpha,
+                                                  bool prev, double (&hc)[KIND == 0 ? 1 : 4]) {
+  constexpr int N = 4, NPE = 64, L = 16, DIM = 3;
+  constexpr int NV = KIND == 0 ? 1 : 4;
+  constexpr int CHUNK = NV * NPE;
+  constexpr bool LAST = BM != 0;
+  using G = Geo<3, 4, KIND>;
+  const int C0 = p.cells[0], C1 = p.cells[1], C2 = p.cells[2];
+  const size_t ebase = (size_t)e * CHUNK;
+  const double a2 = KIND == 1 ? p.sound_speed : 0.0;
+
+  // flux of U along axis d and the one-sided speed (models.cpp:42-70), contracted
+  auto fluxd = [&](const double* U, int d, double* F, double& sp) {
+    if (KIND == 0) {
+      const double vd = d == 0 ? p.vel[0] : (d == 1 ? p.vel[1] : p.vel[2]);
+      F[0] = vd * U[0];
+      sp = fabs(vd);
+    } else {
+      const double rinv = fast_rcp(U[0]);
+      // m_d by value selects (d is a run-time value in the x/y round: an
+      // address select would put the line arrays in local memory)
+      double md = U[1];
+      if (d == 1) md = U[2];
+      if (d == 2) md = U[NV - 1];
+      const double ua = md * rinv;
+      const double pr = U[0] * a2 * a2;
+      F[0] = md;
+#pragma unroll
+      for (int q = 1; q < NV; ++q) F[q] = fma(ua, U[q], q == 1 + d ? pr : 0.0);  // (no U[1 + d] index)
+      sp = fabs(ua) + a2;
+    }
+  };
+
+  // ---------------------------------------------------------- 1: nodes (pair 2 lane, 2 lane + 1)
+  const int n0 = 2 * lane;
+  const int kz0 = n0 >> 4;
+  const int u0s = sw3(n0) & ~1;   // the pair's 16-byte unit in the slab
+  const bool swp = (kz0 & 1) != 0;  // ... with its halves swapped
+  double* sS = sD + 3 * NV * NPE;  // last stage: S at the node pairs (slab, not registers)
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const size_t g = ebase + v * NPE + n0;
+    double2 k[1 + NU];
+    k[0] = __ldg(reinterpret_cast<const double2*>(p.u + g));
+#pragma unroll
+    for (int t = 0; t < NU; ++t) k[1 + t] = __ldg(reinterpret_cast<const double2*>(p.ku[t] + g));
+    double ua = k[0].x, ub = k[0].y;
+#pragma unroll
+    for (int t = 0; t < NU; ++t)
+      if ((AM >> t & 1) != 0) {
+        ua = fma(p.ca[t], k[1 + t].x, ua);
+        ub = fma(p.ca[t], k[1 + t].y, ub);
+      }
+    if (LAST) {
+      double s0 = k[0].x, s1 = k[0].y;
+#pragma unroll
+      for (int t = 0; t < NU; ++t)
+        if ((BM >> t & 1) != 0) {
+          s0 = fma(p.cb[t], k[1 + t].x, s0);
+          s1 = fma(p.cb[t], k[1 + t].y, s1);
+        }
+      *reinterpret_cast<double2*>(sS + v * NPE + n0) = make_double2(s0, s1);
+    }
+    if (KIND == 1 && v == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!((h ? ub : ua) > 0.0)) {
+          const int n = n0 + h, i = n & 3, j = (n >> 2) & 3, kk = n >> 4;
+          const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
+          record_error(p.ctl, error_key(step, p.phase, (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz,
+                                        (j * N + kk) * N + i));
+        }
+      }
+    }
+    *reinterpret_cast<double2*>(sU + v * NPE + u0s) = swp ? make_double2(ub, ua) : make_double2(ua, ub);
+  }
+  __syncwarp();
+
+  // ---------------------------------------------------------- 2: line tasks
+  // task (d, t): line t of axis d; lanes 0-15 x, 16-31 y, then lanes 0-15 z
+  auto line_task = [&](const int d, const int t, const bool reuse_lo) {
+    // the line's end nodes first (their fluxes serve the faces), the inner two after
+    double Ul[4][NV], F[4][NV], sp[4];
+#pragma unroll
+    for (int q = 0; q < 4; q += 3) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Ul[q][v] = sU[v * NPE + sw3(G::node(d, t, q))];
+      fluxd(Ul[q], d, F[q], sp[q]);
+    }
+    // the line's end faces: lo (side 0) at q = 0, hi (side 1) at q = 3
+    double H[2][NV];
+    const int ca = d == 0 ? cx : (d == 1 ? cy : cz);
+    const int cn = d == 0 ? C0 : (d == 1 ? C1 : C2);
+    const int stride = d == 0 ? 1 : (d == 1 ? C0 : C0 * C1);
+    // LF flux at the end face `side` (0: lo, own node q = 0; 1: hi, q = 3)
+    auto end_face = [&](const int side, const double* Uo, const double* Fo, const double so, double* Hs) {
+      const bool bnd = side ? (ca == cn - 1) : (ca == 0);
+      const double* ext = d == 0 ? p.ext[0][side] : (d == 1 ? p.ext[1][side] : p.ext[2][side]);
+      double Un[NV];
+      if (bnd && ext != nullptr) {
+        const size_t xs = d == 0 ? (size_t)cy + (size_t)C1 * cz
+                                 : (d == 1 ? (size_t)cx + (size_t)C0 * cz : (size_t)cx + (size_t)C0 * cy);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) Un[v] = __ldg(ext + (xs * NV + v) * L + t);
+      } else {
+        const int en = side ? (bnd ? e - (cn - 1) * stride : e + stride) : (bnd ? e + (cn - 1) * stride : e - stride);
+        const size_t g = (size_t)en * CHUNK + G::node(d, t, side ? 0 : N - 1);
+        // combined as the loads arrive (the scheduler keeps as many in
+        // flight as the register cap allows)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          Un[v] = __ldg(p.u + g + v * NPE);
+#pragma unroll
+          for (int a = 0; a < NU; ++a)
+            if ((AM >> a & 1) != 0) Un[v] = fma(p.ca[a], __ldg(p.ku[a] + g + v * NPE), Un[v]);
+        }
+      }
+      double Fn[NV], sn;
+      fluxd(Un, d, Fn, sn);
+      const double al = dmax(so, sn);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        // minus state = lower cell along d (solver.cpp:268-306; models.cpp:77-88)
+        const double um = side ? Uo[v] : Un[v], up = side ? Un[v] : Uo[v];
+        const double fm = side ? Fo[v] : Fn[v], fp = side ? Fn[v] : Fo[v];
+        // explicit roundings: the same bits from either side of the face
+        Hs[v] = __dmul_rn(0.5, fma(-al, __dsub_rn(up, um), __dadd_rn(fm, fp)));
+      }
+    };
+    if (reuse_lo) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) H[0][v] = hc[v];
+    } else {
+      end_face(0, Ul[0], F[0], sp[0], H[0]);
+    }
+    end_face(1, Ul[3], F[3], sp[3], H[1]);
+#pragma unroll
+    for (int q = 1; q < 3; ++q) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Ul[q][v] = sU[v * NPE + sw3(G::node(d, t, q))];
+      fluxd(Ul[q], d, F[q], sp[q]);
+    }
+    // D_d = r_d (K_0 F + lifted end fluxes), K_d = r_d K_0 with r_d = lift_d / lift_0
+    const double rd = d == 0 ? 1.0 : (d == 1 ? p.lift[1] : p.lift[2]) / p.lift[0];
+    double* out = sD + d * NV * NPE;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double acc = p.K[0][k * 4] * F[0][v];
+#pragma unroll
+        for (int l = 1; l < 4; ++l) acc = fma(p.K[0][k * 4 + l], F[l][v], acc);
+        if (k == 0) acc = fma(p.lift[0], H[0][v], acc);
+        if (k == 3) acc = fma(-p.lift[0], H[1][v], acc);
+        out[v * NPE + sw3(G::node(d, t, k))] = d == 0 ? acc : acc * rd;
+      }
+    if (d == 2) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) hc[v] = H[1][v];  // the next z element's lo-face flux
+    }
+  };
+  line_task(lane >> 4, lane & 15, false);
+  __syncwarp();  // keeps the two rounds apart in the schedule (their live sets do not add up)
+  if (lane < 16) line_task(2, lane, prev);
+  __syncwarp();
+
+  // ---------------------------------------------------------- 3: epilogue at the node pair
+  double un[2][NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double dv[2];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double2 w = *reinterpret_cast<const double2*>(sD + (d * NV + v) * NPE + u0s);
+      const double w0 = swp ? w.y : w.x, w1 = swp ? w.x : w.y;
+      dv[0] = d == 0 ? w0 : dv[0] + w0;
+      dv[1] = d == 0 ? w1 : dv[1] + w1;
+    }
+    const double k0 = dv[0] * dt, k1 = dv[1] * dt;
+    double* gout = p.out + ebase + v * NPE + n0;
+    if (!LAST) {
+      *reinterpret_cast<double2*>(gout) = make_double2(k0, k1);
+    } else {
+      const double2 S = *reinterpret_cast<const double2*>(sS + v * NPE + n0);
+      un[0][v] = fma(p.b_last, k0, S.x);
+      un[1][v] = fma(p.b_last, k1, S.y);
+      *reinterpret_cast<double2*>(gout) = make_double2(un[0][v], un[1][v]);
+    }
+  }
+  if (LAST) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double sum = un[h][0];
+#pragma unroll
+      for (int v = 1; v < NV; ++v) sum += un[h][v];
+      if (!isfinite(sum)) record_error(p.ctl, error_key(step, kPhaseInstability, p.block_id, 0));
+      if (KIND == 1 && p.scan_alpha) {
+        if (!(un[h][0] > 0.0)) {
+          const long long gx = cx + p.goff[0], gy = cy + p.goff[1], gz = cz + p.goff[2];
+          record_error(p.ctl, error_key(step + 1, kPhaseScan, (gx * p.gcells[1] + gy) * (long long)p.gcells[2] + gz,
+                                        G::aos_node(n0 + h)));
+        } else {
+          double mm = 0.0;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) mm = dmax(mm, fabs(un[h][1 + d]));
+          alpha = dmax(alpha, __dadd_rn(__ddiv_rn(mm, un[h][0]), p.sound_speed));  // == alpha_scan_kernel
+        }
+      }
+    }
+  }
+  __syncwarp();  // this element's slab reads precede the next element's writes
+}
+
 // ------------------------------------------------------------ flagship body
 // One element of the 2D, N = 8, contracted-arithmetic stage (the benchmark
 // shape), written for issue efficiency: lane constants are hoisted by the
@@ -842,23 +1090,24 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
 // Resident CTAs per SM the register allocation is capped for (4 warps each):
 // 4 (<= 128 registers, 16 warps) by default -- capping at 80 for 24 warps
 // measured 25% slower on the flagship (less load-level parallelism per warp).
-// The 3D order-4 Euler tensor-core body (C4) is measured per signature: the
-// u-only stage 5 (4.42 vs 4.55 ms), the one-term and the 2..5-term RK6 stages
-// 3 (<= 168 registers: a face node's loads of every K_j stay in flight;
-// 5.70-9.31 vs 6.02-20.7 ms), the last stage 4 (11.55 vs 12.79 ms).
+// The 3D order-4 Euler line body (C4) is measured per signature
+// (profiles/r02/c4_lines_regcap*.jsonl, caps 2/3/4 everywhere): 4 for the
+// u-only and 1..3-term RK6 stages (3.49 / 4.75 / 5.24 / 6.31 ms), 3 (<= 168
+// registers) for the 4- and 5-term stages (7.07 / 8.13 ms) and 2 (<= 255) for
+// the 7-array last stage (10.52 vs 11.18 at 3 and 13.24 at 4).
 __host__ __device__ constexpr int stage_minb(int dim, int n, int kind, bool exact, int sig) {
 #ifdef NDGX_MINB
   return NDGX_MINB + 0 * (dim + n + kind + (exact ? 1 : 0) + sig);
 #else
 #ifndef NDGX_MINB3
-#define NDGX_MINB3 0x435  // per signature class, hex digits: last stage | many-term | u-only
+#define NDGX_MINB3 0x233443344ull  // per signature, one hex digit each (sig 8 ... sig 0)
 #endif
 #ifndef NDGX_MINB2
 #define NDGX_MINB2 0x444  // the 2D order-8 Euler flagship, same classes: last (bm != 0) | others | u-only
 #endif
   // (generic bodies: 2D o4 5 CTAs, 1.03e11 -> 1.05e11 Euler; 2D o6 Euler 3 CTAs, 7.2e10 -> 7.9e10)
   return (dim == 3 && n == 4 && kind == 1 && !exact)
-             ? (sig == 0 ? (NDGX_MINB3 & 15) : (sig == 8 ? (NDGX_MINB3 >> 8 & 15) : (NDGX_MINB3 >> 4 & 15)))
+             ? (int)((NDGX_MINB3 >> (4 * sig)) & 15)
          : (dim == 2 && n == 8 && kind == 1 && !exact)
              ? (sig == 0 ? (NDGX_MINB2 & 15)
                          : ((kSigs[sig].bm != 0) ? (NDGX_MINB2 >> 8 & 15) : (NDGX_MINB2 >> 4 & 15)))
@@ -967,6 +1216,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 
   // MMA lane roles (2D N=8): lane = 4r + c
   const int r = lane >> 2, c = lane & 3;
+  double hc3[KIND == 0 ? 1 : 4] = {};  // line body: the z-hi face flux carried along a z-run
   Lane4 ln4{};
   if constexpr (USE_MMA3) {
     for (int d = 0; d < 3; ++d) ln4.k[d] = r < 4 ? p.K[d][r * 4 + c] : 0.0;
@@ -1280,7 +1530,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       const int w0 = (int)blockIdx.x * G::WARPS + wib;
       auto visit = [&](int x, int y, int z, bool prev, int par) {
         const int ee = x + C0 * (y + C1 * z);
-        if constexpr (USE_MMA3)
+        if constexpr (USE_MMA3 && NDGX_LINES3 != 0)
+          element_3d4_lines<KIND, NU, AM, BM>(p, lane, ee, x, y, z, sF, sF + NV * NPE, dt, step, alpha,
+                                              NDGX_RUN3 == 2 && NDGX_REUSE3 != 0 && prev, hc3);
+        else if constexpr (USE_MMA3)
           element_3d4_fast<KIND, NU, AM, BM, NDGX_RUN3 == 2 ? 2 : 0>(p, ln4, lane, ee, x, y, z, sF, sT, sH, dt, step,
                                                                     alpha, NDGX_REUSE3 != 0 && prev, par);
         else
@@ -1357,7 +1610,11 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       step_coords(cx, cy, cz);
       continue;
     }
-    if constexpr (USE_MMA3) {
+    if constexpr (USE_MMA3 && NDGX_LINES3 != 0) {
+      element_3d4_lines<KIND, NU, AM, BM>(p, lane, e, cx, cy, cz, sF, sF + NV * NPE, dt, step, alpha, false, hc3);
+      step_coords(cx, cy, cz);
+      continue;
+    } else if constexpr (USE_MMA3) {
       element_3d4_fast<KIND, NU, AM, BM>(p, ln4, lane, e, cx, cy, cz, sF, sT, sH, dt, step, alpha);
       step_coords(cx, cy, cz);
       continue;
