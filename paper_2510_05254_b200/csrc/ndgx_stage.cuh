@@ -614,7 +614,7 @@ __device__ __forceinline__ int sw3(int n) {
 template <int KIND, int NU, int AM, int BM>
 __device__ __forceinline__ void element_3d4_lines(const StageArgs& p, int lane, int e, int cx, int cy, int cz,
                                                   double* sU, double* sD, double dt, long long step, double& alpha,
-                                                  bool prev, double (&hc)[KIND == 0 ? 1 : 4]) {
+                                                  bool prev, double (&hc)[KIND == 0 ? 1 : 4], double rdy, double rdz) {
   constexpr int N = 4, NPE = 64, L = 16, DIM = 3;
   constexpr int NV = KIND == 0 ? 1 : 4;
   constexpr int CHUNK = NV * NPE;
@@ -648,9 +648,7 @@ __device__ __forceinline__ void element_3d4_lines(const StageArgs& p, int lane, 
 
   // ---------------------------------------------------------- 1: nodes (pair 2 lane, 2 lane + 1)
   const int n0 = 2 * lane;
-  const int kz0 = n0 >> 4;
-  const int u0s = sw3(n0) & ~1;   // the pair's 16-byte unit in the slab
-  const bool swp = (kz0 & 1) != 0;  // ... with its halves swapped
+  const int s0 = sw3(n0), s1 = sw3(n0 + 1);  // the pair's slab slots (one 16-byte unit, halves swapped for odd k)
   double* sS = sD + 3 * NV * NPE;  // last stage: S at the node pairs (slab, not registers)
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
@@ -687,19 +685,21 @@ __device__ __forceinline__ void element_3d4_lines(const StageArgs& p, int lane, 
         }
       }
     }
-    *reinterpret_cast<double2*>(sU + v * NPE + u0s) = swp ? make_double2(ub, ua) : make_double2(ua, ub);
+    sU[v * NPE + s0] = ua;  // two 8-byte stores: cheaper than selecting the halves
+    sU[v * NPE + s1] = ub;
   }
   __syncwarp();
 
   // ---------------------------------------------------------- 2: line tasks
   // task (d, t): line t of axis d; lanes 0-15 x, 16-31 y, then lanes 0-15 z
-  auto line_task = [&](const int d, const int t, const bool reuse_lo) {
+  // off[q]: slab slot of the line's node at position q; rd = lift_d / lift_0
+  auto line_task = [&](const int d, const int t, const int (&off)[4], const double rd, const bool reuse_lo) {
     // the line's end nodes first (their fluxes serve the faces), the inner two after
     double Ul[4][NV], F[4][NV], sp[4];
 #pragma unroll
     for (int q = 0; q < 4; q += 3) {
 #pragma unroll
-      for (int v = 0; v < NV; ++v) Ul[q][v] = sU[v * NPE + sw3(G::node(d, t, q))];
+      for (int v = 0; v < NV; ++v) Ul[q][v] = sU[v * NPE + off[q]];
       fluxd(Ul[q], d, F[q], sp[q]);
     }
     // the line's end faces: lo (side 0) at q = 0, hi (side 1) at q = 3
@@ -752,11 +752,10 @@ __device__ __forceinline__ void element_3d4_lines(const StageArgs& p, int lane, 
 #pragma unroll
     for (int q = 1; q < 3; ++q) {
 #pragma unroll
-      for (int v = 0; v < NV; ++v) Ul[q][v] = sU[v * NPE + sw3(G::node(d, t, q))];
+      for (int v = 0; v < NV; ++v) Ul[q][v] = sU[v * NPE + off[q]];
       fluxd(Ul[q], d, F[q], sp[q]);
     }
     // D_d = r_d (K_0 F + lifted end fluxes), K_d = r_d K_0 with r_d = lift_d / lift_0
-    const double rd = d == 0 ? 1.0 : (d == 1 ? p.lift[1] : p.lift[2]) / p.lift[0];
     double* out = sD + d * NV * NPE;
 #pragma unroll
     for (int v = 0; v < NV; ++v)
@@ -767,16 +766,27 @@ __device__ __forceinline__ void element_3d4_lines(const StageArgs& p, int lane, 
         for (int l = 1; l < 4; ++l) acc = fma(p.K[0][k * 4 + l], F[l][v], acc);
         if (k == 0) acc = fma(p.lift[0], H[0][v], acc);
         if (k == 3) acc = fma(-p.lift[0], H[1][v], acc);
-        out[v * NPE + sw3(G::node(d, t, k))] = d == 0 ? acc : acc * rd;
+        out[v * NPE + off[k]] = acc * rd;  // rd == 1 exactly on equal spacing
       }
     if (d == 2) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) hc[v] = H[1][v];  // the next z element's lo-face flux
     }
   };
-  line_task(lane >> 4, lane & 15, false);
+  {
+    // round 1: x line t = j + 4k at slots 16k + 4(j^k) + (q^k); y line t = i + 4k at 16k + 4(q^k) + (i^k)
+    const int d = lane >> 4, t = lane & 15, c = t >> 2, w = t & 3;
+    const int base = 16 * c + (d == 0 ? 4 * (w ^ c) : (w ^ c)), m = d == 0 ? 1 : 4;
+    const int off[4] = {base + m * c, base + m * (1 ^ c), base + m * (2 ^ c), base + m * (3 ^ c)};
+    line_task(d, t, off, d == 0 ? 1.0 : rdy, false);
+  }
   __syncwarp();  // keeps the two rounds apart in the schedule (their live sets do not add up)
-  if (lane < 16) line_task(2, lane, prev);
+  if (lane < 16) {
+    // round 2: z line t = i + 4j at slots 16q + 4(j^q) + (i^q)
+    const int i = lane & 3, j = lane >> 2;
+    const int off[4] = {4 * j + i, 16 + 4 * (j ^ 1) + (i ^ 1), 32 + 4 * (j ^ 2) + (i ^ 2), 48 + 4 * (j ^ 3) + (i ^ 3)};
+    line_task(2, lane, off, rdz, prev);
+  }
   __syncwarp();
 
   // ---------------------------------------------------------- 3: epilogue at the node pair
@@ -786,8 +796,7 @@ __device__ __forceinline__ void element_3d4_lines(const StageArgs& p, int lane, 
     double dv[2];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const double2 w = *reinterpret_cast<const double2*>(sD + (d * NV + v) * NPE + u0s);
-      const double w0 = swp ? w.y : w.x, w1 = swp ? w.x : w.y;
+      const double w0 = sD[(d * NV + v) * NPE + s0], w1 = sD[(d * NV + v) * NPE + s1];
       dv[0] = d == 0 ? w0 : dv[0] + w0;
       dv[1] = d == 0 ? w1 : dv[1] + w1;
     }
@@ -1090,17 +1099,18 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
 // Resident CTAs per SM the register allocation is capped for (4 warps each):
 // 4 (<= 128 registers, 16 warps) by default -- capping at 80 for 24 warps
 // measured 25% slower on the flagship (less load-level parallelism per warp).
-// The 3D order-4 Euler line body (C4) is measured per signature
-// (profiles/r02/c4_lines_regcap*.jsonl, caps 2/3/4 everywhere): 4 for the
-// u-only and 1..3-term RK6 stages (3.49 / 4.75 / 5.24 / 6.31 ms), 3 (<= 168
-// registers) for the 4- and 5-term stages (7.07 / 8.13 ms) and 2 (<= 255) for
-// the 7-array last stage (10.52 vs 11.18 at 3 and 13.24 at 4).
+// The 3D order-4 Euler line body (C4) is measured per signature, per-stage
+// minima of repeated runs at caps 2..5 (profiles/r02/c4_lines_regcap3.jsonl):
+// 5 (<= 96 registers, 20 warps) for the u-only, 1- and 2-term RK6 stages
+// (3.55 / 4.24 / 5.36 ms), 4 for the 3- and 4-term stages (6.49 / 7.49), 2
+// (<= 255 registers: every K_j load of a face node in flight) for the 5-term
+// and the 7-array last stage (9.01 / 10.64 ms, vs 9.29 / 11.19 at 3).
 __host__ __device__ constexpr int stage_minb(int dim, int n, int kind, bool exact, int sig) {
 #ifdef NDGX_MINB
   return NDGX_MINB + 0 * (dim + n + kind + (exact ? 1 : 0) + sig);
 #else
 #ifndef NDGX_MINB3
-#define NDGX_MINB3 0x233443344ull  // per signature, one hex digit each (sig 8 ... sig 0)
+#define NDGX_MINB3 0x224453355ull  // per signature, one hex digit each (sig 8 ... sig 0)
 #endif
 #ifndef NDGX_MINB2
 #define NDGX_MINB2 0x444  // the 2D order-8 Euler flagship, same classes: last (bm != 0) | others | u-only
@@ -1217,6 +1227,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   // MMA lane roles (2D N=8): lane = 4r + c
   const int r = lane >> 2, c = lane & 3;
   double hc3[KIND == 0 ? 1 : 4] = {};  // line body: the z-hi face flux carried along a z-run
+  const double rdy3 = DIM == 3 ? p.lift[1] / p.lift[0] : 1.0, rdz3 = DIM == 3 ? p.lift[2] / p.lift[0] : 1.0;
   Lane4 ln4{};
   if constexpr (USE_MMA3) {
     for (int d = 0; d < 3; ++d) ln4.k[d] = r < 4 ? p.K[d][r * 4 + c] : 0.0;
@@ -1532,7 +1543,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         const int ee = x + C0 * (y + C1 * z);
         if constexpr (USE_MMA3 && NDGX_LINES3 != 0)
           element_3d4_lines<KIND, NU, AM, BM>(p, lane, ee, x, y, z, sF, sF + NV * NPE, dt, step, alpha,
-                                              NDGX_RUN3 == 2 && NDGX_REUSE3 != 0 && prev, hc3);
+                                              NDGX_RUN3 == 2 && NDGX_REUSE3 != 0 && prev, hc3, rdy3, rdz3);
         else if constexpr (USE_MMA3)
           element_3d4_fast<KIND, NU, AM, BM, NDGX_RUN3 == 2 ? 2 : 0>(p, ln4, lane, ee, x, y, z, sF, sT, sH, dt, step,
                                                                     alpha, NDGX_REUSE3 != 0 && prev, par);
@@ -1611,7 +1622,8 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       continue;
     }
     if constexpr (USE_MMA3 && NDGX_LINES3 != 0) {
-      element_3d4_lines<KIND, NU, AM, BM>(p, lane, e, cx, cy, cz, sF, sF + NV * NPE, dt, step, alpha, false, hc3);
+      element_3d4_lines<KIND, NU, AM, BM>(p, lane, e, cx, cy, cz, sF, sF + NV * NPE, dt, step, alpha, false, hc3, rdy3,
+                                          rdz3);
       step_coords(cx, cy, cz);
       continue;
     } else if constexpr (USE_MMA3) {
