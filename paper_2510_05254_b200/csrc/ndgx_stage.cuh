@@ -63,9 +63,6 @@ struct Geo {
   static constexpr int FN = FACES * L;                                // face nodes per element
   static constexpr int FM = (FN + 31) / 32;                           // face nodes per lane
   static constexpr int HW = 2 * NV + 1;                               // trace: U[NV], F[NV], speed
-  static constexpr int WARPS = 4;                                     // warps per CTA
-  static constexpr int THREADS = 32 * WARPS;
-  static constexpr int MAXD = 4;                                      // max ring depth per warp
   // shared memory: [mbarriers WARPS*MAXD][scratch RED] then per warp a slab
   // (doubles): fluxes [DIM][NV][NPE] | traces [face][HW][L] | face fluxes
   // [face][NV][L], followed by the warp's ring of D element slots, each
@@ -73,6 +70,11 @@ struct Geo {
   static constexpr int OFF_T = DIM * NV * NPE;
   static constexpr int OFF_H = OFF_T + FACES * HW * L;
   static constexpr int WSLAB = ((OFF_H + FACES * NV * L) + 1) & ~1;
+  // warps per CTA: 4, fewer where four generic slabs exceed ~190 KB (3D
+  // order 7: 3 warps, order 8: 2 -- one element is 63 / 89 KB of slab)
+  static constexpr int WARPS = WSLAB * 4 <= 24000 ? 4 : (24000 / WSLAB < 1 ? 1 : 24000 / WSLAB);
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int MAXD = 4;                                      // max ring depth per warp
   static constexpr int RED = 2 * WARPS;                      // block reduction scratch (doubles)
   static constexpr int HEAD = WARPS * MAXD + RED;            // 8-byte words before the slabs
   static constexpr int CHUNK = NV * NPE;                     // one array of one element (doubles)
@@ -1520,7 +1522,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 #define NDGX_RUN3 2  // 3D traversal of whole-plane launches: 0 element order, 1 x-runs, 2 z-runs
 #endif
 #ifndef NDGX_RUNLEN3
-#define NDGX_RUNLEN3 16
+#define NDGX_RUNLEN3 8  // z-run length: DRAM bytes per C4 step 1.13x the algorithmic (1.17x at 16, 1.12x at 4), same time
 #endif
 #ifndef NDGX_YB3
 #define NDGX_YB3 8

@@ -239,3 +239,39 @@ def test_full_size_c3_rhs_bitwise_and_step_properties(port):
     d = ue - uf
     for v in range(3):
         assert np.sqrt((d[v::3] ** 2).sum() / (ue[v::3] ** 2).sum()) <= REL_L2_TOL
+
+
+# Every (dim, order, equation) kernel instance the registry compiles, on a tiny
+# mesh against the oracle port: exact bitwise, fast within REL_L2_TOL.  This
+# covers the bodies and lane groupings the golden cases do not name (2D o6,
+# 1D o3/o5-o7, 3D o5-o8, the 3D line body under RK3/RK4 ...).
+SHAPES = ([(1, o, ADVECTION) for o in range(2, 9)] + [(2, o, k) for o in range(2, 9) for k in (ADVECTION, EULER)] +
+          [(3, o, k) for o in range(2, 9) for k in (ADVECTION, EULER)])
+CELLS = {1: (9,), 2: (5, 4), 3: (3, 2, 3)}
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"{s[0]}D-o{s[1]}-{'euler' if s[2] == EULER else 'adv'}")
+def test_every_shape_matches_port(port, shape):
+    dim, order, kind = shape
+    rk = (RK3, RK4, RK6)[order % 3]
+    p = Problem(dim, CELLS[dim], order, kind, rk, velocity=(1.0, -0.5, 0.25), sound_speed=1.0)
+    cfg = config_of(p)
+    if kind == EULER:
+        u0 = ndgx.init_euler_subsonic(cfg.mesh, cfg.model)
+    else:
+        u0 = ndgx.init_multisine(cfg.mesh, cfg.model, n_modes=3, seed=5)
+    steps = 3
+    want, want_st = port.advance(p, u0, steps)
+    r_want = port.rhs(p, u0)
+    for arith in (ndgx.ARITH_EXACT, ndgx.ARITH_FAST):
+        with ndgx.Solver(cfg, arith=arith) as s:
+            s.upload(u0)
+            r0 = s.rhs()
+            st = s.advance(ndgx.StepPlan(steps, False))
+            uf = s.download()
+        if arith == ndgx.ARITH_EXACT:
+            assert np.array_equal(r0, r_want) and np.array_equal(uf, want)
+            assert st.dt_min == want_st.dt_min and st.dt_max == want_st.dt_max
+        else:
+            assert max(rel_l2(port, p, r0, r_want)) <= REL_L2_TOL
+            assert max(rel_l2(port, p, uf, want)) <= REL_L2_TOL
