@@ -375,7 +375,7 @@ def bench_ours(args):
     bytes_per_launch = BYTES_PER_DOF_STAGE[rk] * dof
     peak, peak_src = measured_peaks()
     achieved = bytes_per_launch / (avg_stage_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, ""
     prof_path = os.path.join(ROOT, "profiles", "ncu_stage_traffic.json")
     if os.path.exists(prof_path):
         with open(prof_path) as f:
@@ -383,6 +383,7 @@ def bench_ours(args):
         tr = prof.get(args.config, {}).get(args.arith)
         if tr:
             traffic = tr.get("dram_bytes_per_launch")
+            traffic_src = tr.get("source", "")
 
     # ---- sharded roofline (N > 1): HBM time vs halo time over NVLink ----
     sharded = None
@@ -498,8 +499,9 @@ def bench_ours(args):
                        "l2": L2_NOTE[args.config]},
             "roofline": {"bound": sharded["bound"] if sharded else "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "traffic_source": "profiles/ncu_stage_traffic.json (ncu dram__bytes_read.sum + "
-                                           "dram__bytes_write.sum per stage launch, same kernel), not this run",
+                         "traffic_source": "profiles/ncu_stage_traffic.json: ncu dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum averaged over the stage launches of one step, "
+                                           "measured on the same kernel build, not in this run (" + traffic_src + ")",
                          "kernel": "ndgx::stage_kernel (fused NDG RHS + RK stage)",
                          "bytes_per_dof_stage": BYTES_PER_DOF_STAGE[rk],
                          "avg_launch_ms": avg_stage_ms, "stage_ms": stage_ms.tolist(), "step_control_ms": ctl_ms,
