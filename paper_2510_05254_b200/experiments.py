@@ -10,10 +10,11 @@ states are bit-identical to the reference's, and so are the L2 errors,
 slopes and fit constants: tests/test_experiments.py checks whole reports
 against the reference's own run_converge / run_fit / run_timing.
 
-Multi-GPU rows (workers > 1) come from bench.py under torchrun; a spec
-asking for more workers than this single-GPU driver runs gets the
-reference's "skipped" row (DecompositionError), like a worker count the
-reference cannot decompose.
+Rows with workers > 1 go through run_partitioned (src/partition.cpp:186-333,
+timed_run's own multi-worker branch): the worker count's decompose() blocks
+in one partitioned handle, block w on devices[w % len(devices)].  A worker
+count the mesh cannot be decomposed into gets the reference's "skipped" row
+(DecompositionError); a failing run its "failed" row.
 """
 from __future__ import annotations
 
@@ -125,16 +126,19 @@ def fill_stats(row: BenchRow, stats: ndgx.StepStats) -> None:
 
 @dataclass
 class Runner:
-    """Where timed_run's solves go: one GPU, in ``arith`` mode."""
+    """Where timed_run's solves go: GPUs ``devices`` (default [device]), in ``arith`` mode."""
     device: int = 0
     arith: int = ndgx.ARITH_EXACT
+    devices: Optional[List[int]] = None
 
     def timed_run(self, config: ndgx.SolverConfig, initial, plan: ndgx.StepPlan, workers: int):
-        """timed_run (src/experiments.cpp:82-90) on the GPU."""
-        if workers > 1:
-            raise ndgx.DecompositionError(
-                f"{workers} workers: multi-GPU runs go through bench.py under torchrun (one rank per GPU)")
-        r = ndgx.advance(config, initial, plan, device=self.device, arith=self.arith)
+        """timed_run (src/experiments.cpp:82-90) on the GPU: advance for one
+        worker, run_partitioned for more."""
+        if workers <= 1:
+            r = ndgx.advance(config, initial, plan, device=self.device, arith=self.arith)
+            return r.state, r.stats
+        r = ndgx.run_partitioned(config, initial, workers, plan, devices=self.devices or [self.device],
+                                 arith=self.arith)
         return r.state, r.stats
 
 

@@ -110,17 +110,28 @@ def test_l2_error_and_totals_bit_identical_to_the_reference(reference, dim, cell
         ndgx.l2_error(mesh, model, a, b, model.n_var())
 
 
-def test_single_gpu_driver_skips_multi_worker_timing_rows():
-    spec = ex.ExperimentSpec("timing", "euler", 2, [4], "rk4", [4], workers=[2], steps=2)
+def test_multi_worker_timing_rows_skip_undecomposable_meshes():
+    # timed_run's multi-worker branch is run_partitioned: a worker count the
+    # mesh cannot be split into is the reference's "skipped" row (decided on
+    # the host, before any device work)
+    spec = ex.ExperimentSpec("timing", "euler", 2, [4], "rk4", [1], workers=[3], steps=2)
+    rows = ex.run_timing(spec, ex.Runner()).rows
+    assert [r.status for r in rows] == ["skipped"] and rows[0].workers == 3
 
-    class NoGpu(ex.Runner):
-        def timed_run(self, *a):  # the worker check fires before any device work
-            return ex.Runner.timed_run(self, *a)
 
-    rows = ex.run_timing(spec, NoGpu()).rows
-    assert [r.status for r in rows] == ["skipped"] and "torchrun" in rows[0].note
+def test_scale_driver_is_not_on_the_gpu_path():
     with pytest.raises(ndgx.ConfigError, match="not on the GPU path"):
         ex.run_experiment(ex.ExperimentSpec("scale"))
+
+
+@pytest.mark.gpu
+def test_multi_worker_timing_rows_run_partitioned():
+    # workers = 2: the partitioned handle; states bit-identical to one worker,
+    # so every non-timing column equals the single-worker row
+    one = ex.run_timing(ex.ExperimentSpec("timing", "euler", 2, [4], "rk4", [6], steps=3)).rows[0]
+    two = ex.run_timing(ex.ExperimentSpec("timing", "euler", 2, [4], "rk4", [6], workers=[2], steps=3)).rows[0]
+    assert two.status == "ok" and two.workers == 2
+    assert (two.steps, two.dt_min, two.dt_max, two.dof) == (one.steps, one.dt_min, one.dt_max, one.dof)
 
 
 # ------------------------------------------------------------------ GPU
