@@ -616,7 +616,8 @@ __device__ __forceinline__ int sw3(int n) {
 template <int KIND, int NU, int AM, int BM>
 __device__ __forceinline__ void element_3d4_lines(const StageArgs& p, int lane, int e, int cx, int cy, int cz,
                                                   double* sU, double* sD, double dt, long long step, double& alpha,
-                                                  bool prev, double (&hc)[KIND == 0 ? 1 : 4], double rdy, double rdz) {
+                                                  bool prev, double (&hc)[KIND == 0 ? 1 : 4], double rdy, double rdz,
+                                                  bool scaled) {
   constexpr int N = 4, NPE = 64, L = 16, DIM = 3;
   constexpr int NV = KIND == 0 ? 1 : 4;
   constexpr int CHUNK = NV * NPE;
@@ -768,7 +769,7 @@ __device__ __forceinline__ void element_3d4_lines(const StageArgs& p, int lane, 
         for (int l = 1; l < 4; ++l) acc = fma(p.K[0][k * 4 + l], F[l][v], acc);
         if (k == 0) acc = fma(p.lift[0], H[0][v], acc);
         if (k == 3) acc = fma(-p.lift[0], H[1][v], acc);
-        out[v * NPE + off[k]] = acc * rd;  // rd == 1 exactly on equal spacing
+        out[v * NPE + off[k]] = scaled ? acc * rd : acc;  // (warp-uniform: rd == 1 on equal spacing)
       }
     if (d == 2) {
 #pragma unroll
@@ -783,11 +784,90 @@ __device__ __forceinline__ void element_3d4_lines(const StageArgs& p, int lane, 
     line_task(d, t, off, d == 0 ? 1.0 : rdy, false);
   }
   __syncwarp();  // keeps the two rounds apart in the schedule (their live sets do not add up)
-  if (lane < 16) {
-    // round 2: z line t = i + 4j at slots 16q + 4(j^q) + (i^q)
-    const int i = lane & 3, j = lane >> 2;
-    const int off[4] = {4 * j + i, 16 + 4 * (j ^ 1) + (i ^ 1), 32 + 4 * (j ^ 2) + (i ^ 2), 48 + 4 * (j ^ 3) + (i ^ 3)};
-    line_task(2, lane, off, rdz, prev);
+  {
+    // round 2: the z lines, each split over two lanes: lane t (half 0) the
+    // lo face and outputs q = 0, 1, lane t + 16 (half 1) the hi face and
+    // q = 2, 3; both read the line and form its 4 fluxes.  Line t = i + 4j
+    // sits at slots 16q + 4(j^q) + (i^q).  The z-hi flux carried along the
+    // run lives on the half-1 lane; the half-0 lane takes it by a shuffle.
+    constexpr int d = 2;
+    const int t = lane & 15, half = lane >> 4, i = t & 3, j = t >> 2;
+    double hprev[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) hprev[v] = __shfl_xor_sync(0xffffffffu, hc[v], 16);
+    double Ul[4][NV], F[4][NV], sp[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Ul[q][v] = sU[v * NPE + 16 * q + 4 * (j ^ q) + (i ^ q)];
+      fluxd(Ul[q], d, F[q], sp[q]);
+    }
+    double Uo[NV], Fo[NV];  // this half's end node (value selects: no dynamic index)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      Uo[v] = half ? Ul[3][v] : Ul[0][v];
+      Fo[v] = half ? F[3][v] : F[0][v];
+    }
+    const double so = half ? sp[3] : sp[0];
+    double H[NV];
+    // the lo face of a run's inner element: the carried flux; else computed
+    const bool take = half == 0 && prev;
+    const bool bnd = half ? (cz == C2 - 1) : (cz == 0);
+    const double* ext = half ? p.ext[2][1] : p.ext[2][0];
+    double Un[NV];
+    if (!take) {
+      if (bnd && ext != nullptr) {
+        const size_t xs = (size_t)cx + (size_t)C0 * cy;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) Un[v] = __ldg(ext + (xs * NV + v) * L + t);
+      } else {
+        const int stride = C0 * C1;
+        const int en = half ? (bnd ? e - (C2 - 1) * stride : e + stride) : (bnd ? e + (C2 - 1) * stride : e - stride);
+        const size_t g = (size_t)en * CHUNK + t + (half ? 0 : 48);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          Un[v] = __ldg(p.u + g + v * NPE);
+#pragma unroll
+          for (int a = 0; a < NU; ++a)
+            if ((AM >> a & 1) != 0) Un[v] = fma(p.ca[a], __ldg(p.ku[a] + g + v * NPE), Un[v]);
+        }
+      }
+      double Fn[NV], sn;
+      fluxd(Un, d, Fn, sn);
+      const double al = dmax(so, sn);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        // minus state = lower cell along z (solver.cpp:268-306; models.cpp:77-88)
+        const double um = half ? Uo[v] : Un[v], up = half ? Un[v] : Uo[v];
+        const double fm = half ? Fo[v] : Fn[v], fp = half ? Fn[v] : Fo[v];
+        H[v] = __dmul_rn(0.5, fma(-al, __dsub_rn(up, um), __dadd_rn(fm, fp)));
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (take) H[v] = hprev[v];
+      if (half) hc[v] = H[v];  // the next z element's lo-face flux (taken by lane t)
+    }
+    // outputs q = 2 half + s: K_2 rows by value selects, the own face lifted
+    // onto q = 0 (half 0) or q = 3 (half 1)
+    const double ca0 = half ? 0.0 : p.lift[0], cb1 = half ? -p.lift[0] : 0.0;
+    double* out = sD + d * NV * NPE;
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      double kr[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) kr[l] = half ? p.K[0][(2 + s2) * 4 + l] : p.K[0][s2 * 4 + l];
+      const int q = 2 * half + s2;
+      const int slot = 16 * q + 4 * (j ^ q) + (i ^ q);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double acc = kr[0] * F[0][v];
+#pragma unroll
+        for (int l = 1; l < 4; ++l) acc = fma(kr[l], F[l][v], acc);
+        acc = fma(s2 == 0 ? ca0 : cb1, H[v], acc);
+        out[v * NPE + slot] = scaled ? acc * rdz : acc;
+      }
+    }
   }
   __syncwarp();
 
@@ -1102,17 +1182,17 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
 // 4 (<= 128 registers, 16 warps) by default -- capping at 80 for 24 warps
 // measured 25% slower on the flagship (less load-level parallelism per warp).
 // The 3D order-4 Euler line body (C4) is measured per signature, per-stage
-// minima of repeated runs at caps 2..5 (profiles/r02/c4_lines_regcap3.jsonl):
-// 5 (<= 96 registers, 20 warps) for the u-only, 1- and 2-term RK6 stages
-// (3.55 / 4.24 / 5.36 ms), 4 for the 3- and 4-term stages (6.49 / 7.49), 2
-// (<= 255 registers: every K_j load of a face node in flight) for the 5-term
-// and the 7-array last stage (9.01 / 10.64 ms, vs 9.29 / 11.19 at 3).
+// minima of repeated runs at caps 2..5 (profiles/r02/c4_zsplit_regcap.jsonl):
+// 4 (<= 128 registers, 16 warps) for the u-only and 1..5-term RK6 stages
+// (3.73 / 4.62 / 5.42 / 6.22 / 7.36 / 8.87 ms), 2 (<= 255 registers: every
+// K_j load of a face node in flight) for the 7-array last stage (10.35 ms vs
+// 12.22 at 3 and 13.93 at 4).
 __host__ __device__ constexpr int stage_minb(int dim, int n, int kind, bool exact, int sig) {
 #ifdef NDGX_MINB
   return NDGX_MINB + 0 * (dim + n + kind + (exact ? 1 : 0) + sig);
 #else
 #ifndef NDGX_MINB3
-#define NDGX_MINB3 0x224453355ull  // per signature, one hex digit each (sig 8 ... sig 0)
+#define NDGX_MINB3 0x244443344ull  // per signature, one hex digit each (sig 8 ... sig 0)
 #endif
 #ifndef NDGX_MINB2
 #define NDGX_MINB2 0x444  // the 2D order-8 Euler flagship, same classes: last (bm != 0) | others | u-only
@@ -1230,6 +1310,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   const int r = lane >> 2, c = lane & 3;
   double hc3[KIND == 0 ? 1 : 4] = {};  // line body: the z-hi face flux carried along a z-run
   const double rdy3 = DIM == 3 ? p.lift[1] / p.lift[0] : 1.0, rdz3 = DIM == 3 ? p.lift[2] / p.lift[0] : 1.0;
+  const bool scaled3 = DIM == 3 && !(rdy3 == 1.0 && rdz3 == 1.0);  // unequal spacing: K_d = r_d K_0
   Lane4 ln4{};
   if constexpr (USE_MMA3) {
     for (int d = 0; d < 3; ++d) ln4.k[d] = r < 4 ? p.K[d][r * 4 + c] : 0.0;
@@ -1545,7 +1626,8 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         const int ee = x + C0 * (y + C1 * z);
         if constexpr (USE_MMA3 && NDGX_LINES3 != 0)
           element_3d4_lines<KIND, NU, AM, BM>(p, lane, ee, x, y, z, sF, sF + NV * NPE, dt, step, alpha,
-                                              NDGX_RUN3 == 2 && NDGX_REUSE3 != 0 && prev, hc3, rdy3, rdz3);
+                                              NDGX_RUN3 == 2 && NDGX_REUSE3 != 0 && prev, hc3, rdy3, rdz3,
+                                              scaled3);
         else if constexpr (USE_MMA3)
           element_3d4_fast<KIND, NU, AM, BM, NDGX_RUN3 == 2 ? 2 : 0>(p, ln4, lane, ee, x, y, z, sF, sT, sH, dt, step,
                                                                     alpha, NDGX_REUSE3 != 0 && prev, par);
@@ -1625,7 +1707,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     }
     if constexpr (USE_MMA3 && NDGX_LINES3 != 0) {
       element_3d4_lines<KIND, NU, AM, BM>(p, lane, e, cx, cy, cz, sF, sF + NV * NPE, dt, step, alpha, false, hc3, rdy3,
-                                          rdz3);
+                                          rdz3, scaled3);
       step_coords(cx, cy, cz);
       continue;
     } else if constexpr (USE_MMA3) {
