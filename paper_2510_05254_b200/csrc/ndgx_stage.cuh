@@ -94,6 +94,16 @@ struct Geo {
   static constexpr int GL = group_lanes();
 #endif
   static constexpr int EPW = 32 / GL;
+  // per-group slab stride: WSLAB padded so that the EPW groups' slabs start
+  // 16/EPW doubles apart modulo the 32 banks (with equal alignment every
+  // group hit the same banks: 2D o4 had 40 of 78 shared wavefronts excessive)
+#ifndef NDGX_GPAD
+#define NDGX_GPAD 1
+#endif
+  static constexpr int GSTRIDE =
+      (EPW == 1 || NDGX_GPAD == 0 || DIM == 3) ? WSLAB : WSLAB + ((16 / EPW) - (WSLAB % 16) + 16) % 16;
+  // (measured, profiles/r02/loworder_pad_ab.jsonl: 2D Euler o2 9.4e10 -> 1.03e11, o4 1.05e11 -> 1.19e11,
+  //  o5 +3%; 3D o2 Euler -5%, so 3D keeps the plain stride)
   static constexpr int NMG = (NPE + GL - 1) / GL;            // node passes of a lane
   static constexpr int FMG = (FN + GL - 1) / GL;             // face passes of a lane
   static constexpr bool TMA_OK = (CHUNK % 2) == 0 && GL == 32;  // 16-byte element chunks, one element per warp
@@ -114,7 +124,7 @@ struct Geo {
     return mma ? (MMA3 ? (NDGX_LINES3 ? (4 + (last ? 1 : 0)) * NV * NPE  // line body: U | three dudt parts | S
                                       : (((3 + (last ? 1 : 0)) * NV * NPE + FACES * (NV + 1) * L + FACES * NV * L + 1) & ~1))
                        : (((1 + (last ? 1 : 0)) * NV * NPE + FACES * HW * L + FACES * NV * L + 1) & ~1))
-               : EPW * WSLAB;
+               : EPW * GSTRIDE;
   }
   // which body a (arith, signature) kernel runs: the 2D N=8 / 3D N=4
   // tensor-core bodies (contracted mode; 3D for the NDGX_MMA3_SIGS stages)
@@ -1430,7 +1440,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
                              const double* fsrc, const bool act) {
     constexpr int GL = G::GL;
     const int sub = GL == 32 ? lane : (lane & (GL - 1)), grp = GL == 32 ? 0 : lane / GL;
-    double* const gF = sF + grp * G::WSLAB;
+    double* const gF = sF + grp * G::GSTRIDE;
     double* const gT = gF + G::OFF_T;
     double* const gH = gF + G::OFF_H;
     const size_t ebase = (size_t)e * NV * NPE;

@@ -12,12 +12,17 @@ from bench import CONFIGS  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 arith = ndgx.ARITH_FAST if (len(sys.argv) > 2 and sys.argv[2] == "fast") else ndgx.ARITH_EXACT
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
-dim, cells, order, eq, rk, desc = CONFIGS[name]
+if name in CONFIGS:
+    dim, cells, order, eq, rk, desc = CONFIGS[name]
+else:  # dim:order:eq at ~1e8 DOF, RK4 (order sweeps)
+    dim, order, eq = (int(x) for x in name.split(":"))
+    c = max(4, int(round((1e8 / (order ** dim * ((dim + 1) if eq else 1))) ** (1.0 / dim))))
+    cells, rk, desc = (c,) * dim, 1, f"{dim}D order {order} eq {eq}, {c}^{dim} cells"
+
 mesh = ndgx.Mesh(dim, cells, order)
 model = ndgx.EquationModel.isothermal_euler(dim, 1.0) if eq else ndgx.EquationModel.advection(dim, (1, 0, 0))
-u0 = ndgx.init_euler_subsonic(mesh, model) if eq else ndgx.init_multisine(mesh, model, n_modes=40, seed=42)
 with ndgx.Solver(ndgx.SolverConfig(mesh, model, rk), arith=arith) as s:
-    s.upload(u0)
+    s.init_device(ndgx.IC_EULER_SUBSONIC if eq else ndgx.IC_MULTISINE, None if eq else ndgx.multisine_amplitudes(40, 42))
     st = s.advance(ndgx.StepPlan(steps, False))
     print(desc, "arith", sys.argv[2] if len(sys.argv) > 2 else "exact", "steps", st.steps,
           "ms/step", st.wall_seconds / st.steps * 1e3)
