@@ -46,6 +46,9 @@ namespace ndgx {
 // many-term RK6 stages keep their face loads in flight (C4, 128^3: the 2..5
 // term stages 6.75 / 7.55 / 8.24 / 9.31 ms vs 8.51 / 9.14 / 9.87 / 11.53 ms in
 // the generic body).
+#ifndef NDGX_GEN_UTRACE
+#define NDGX_GEN_UTRACE 1  // generic body: face traces hold U only (flux and speed recomputed at the face)
+#endif
 #ifndef NDGX_LINES3
 #define NDGX_LINES3 1  // 3D order-4 contracted stages: line-task body (1) or the tensor-core body (0)
 #endif
@@ -63,12 +66,13 @@ struct Geo {
   static constexpr int FN = FACES * L;                                // face nodes per element
   static constexpr int FM = (FN + 31) / 32;                           // face nodes per lane
   static constexpr int HW = 2 * NV + 1;                               // trace: U[NV], F[NV], speed
+  static constexpr int TW = NDGX_GEN_UTRACE ? NV : HW;                // generic trace record width (U only)
   // shared memory: [mbarriers WARPS*MAXD][scratch RED] then per warp a slab
   // (doubles): fluxes [DIM][NV][NPE] | traces [face][HW][L] | face fluxes
   // [face][NV][L], followed by the warp's ring of D element slots, each
   // holding u and the NU K_j of one element ([array][var][node], TMA-filled)
   static constexpr int OFF_T = DIM * NV * NPE;
-  static constexpr int OFF_H = OFF_T + FACES * HW * L;
+  static constexpr int OFF_H = OFF_T + FACES * TW * L;
   static constexpr int WSLAB = ((OFF_H + FACES * NV * L) + 1) & ~1;
   // warps per CTA: 4, fewer where four generic slabs exceed ~190 KB (3D
   // order 7: 3 warps, order 8: 2 -- one element is 63 / 89 KB of slab)
@@ -101,9 +105,9 @@ struct Geo {
 #define NDGX_GPAD 1
 #endif
   static constexpr int GSTRIDE =
-      (EPW == 1 || NDGX_GPAD == 0 || DIM == 3) ? WSLAB : WSLAB + ((16 / EPW) - (WSLAB % 16) + 16) % 16;
+      (EPW == 1 || NDGX_GPAD == 0) ? WSLAB : WSLAB + ((16 / EPW) - (WSLAB % 16) + 16) % 16;
   // (measured, profiles/r02/loworder_pad_ab.jsonl: 2D Euler o2 9.4e10 -> 1.03e11, o4 1.05e11 -> 1.19e11,
-  //  o5 +3%; 3D o2 Euler -5%, so 3D keeps the plain stride)
+  //  o5 +3%; with U-only trace records 3D o2 Euler needs it too: its slab became a multiple of 16)
   static constexpr int NMG = (NPE + GL - 1) / GL;            // node passes of a lane
   static constexpr int FMG = (FN + GL - 1) / GL;             // face passes of a lane
   static constexpr bool TMA_OK = (CHUNK % 2) == 0 && GL == 32;  // 16-byte element chunks, one element per warp
@@ -1230,9 +1234,6 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   constexpr bool USE_MMA = G::MMA && !EXACT;
   constexpr bool USE_MMA3 = G::MMA3 && G::mma_body(EXACT, SIG);
   constexpr int NU = kSigs[SIG].nu, AM = kSigs[SIG].am, BM = kSigs[SIG].bm;
-#ifndef NDGX_GEN_UTRACE
-#define NDGX_GEN_UTRACE 1
-#endif
   // generic body: face traces hold U only; the face lane recomputes its own
   // side's flux and speed (fewer partial-warp shared stores)
   constexpr bool GEN_UTRACE = NDGX_GEN_UTRACE != 0;
@@ -1262,7 +1263,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   // slab: fluxes (2D MMA: F_y; 3D MMA: F_x|F_y|F_z) | S (last stage) | traces | face fluxes
   constexpr int OFFT = USE_MMA ? (1 + (LASTC ? 1 : 0)) * NV * NPE
                                : (USE_MMA3 ? (3 + (LASTC ? 1 : 0)) * NV * NPE : G::OFF_T);
-  constexpr int TRW = USE_MMA3 ? NV + 1 : HW;                // trace record width
+  constexpr int TRW = USE_MMA3 ? NV + 1 : (USE_MMA ? HW : G::TW);  // trace record width
   double* sF = smem + G::HEAD + wib * (WSL + depth * SLOT);
   double* sT = sF + OFFT;                                    // [face][TRW][L]
   double* sH = sT + G::FACES * TRW * L;                      // [face][NV][L]
@@ -1481,7 +1482,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         for (int v = 0; v < NV; ++v) gF[(d * NV + v) * NPE + n] = F[v];
         const int k = G::pos_of(d, n);
         if (k == 0 || k == N - 1) {
-          double* t = gT + ((2 * d + (k == 0 ? 0 : 1)) * HW) * L + G::line_of(d, n);
+          double* t = gT + ((2 * d + (k == 0 ? 0 : 1)) * G::TW) * L + G::line_of(d, n);
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
             t[v * L] = U[v];
@@ -1500,7 +1501,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       if (!act || q >= G::FN) continue;
       const int f = q / L, t = q - f * L;
       const int d = f >> 1, side = f & 1;
-      const double* own = gT + (f * HW) * L + t;
+      const double* own = gT + (f * G::TW) * L + t;
       // neighbour across (d, side): periodic wrap in this block, or the received plane
       const int ca = d == 0 ? cx : (d == 1 ? cy : cz);
       const int cn = d == 0 ? C0 : (d == 1 ? C1 : C2);
