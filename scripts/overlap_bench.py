@@ -16,7 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2510_05254_b200 as ndgx  # noqa: E402
 
 arith = ndgx.ARITH_EXACT if (len(sys.argv) > 1 and sys.argv[1] == "exact") else ndgx.ARITH_FAST
-steps = 20
+steps = 20 if not (len(sys.argv) > 2 and sys.argv[2] == "3d") else 4
 
 
 def timed(s, u0):
@@ -31,10 +31,11 @@ def timed(s, u0):
     return best, [round(x, 4) for x in stage]
 
 
-def case(name, cells, variants):
-    mesh = ndgx.Mesh(2, cells, 8)
-    model = ndgx.EquationModel.isothermal_euler(2, 1.0)
-    cfg = ndgx.SolverConfig(mesh, model, ndgx.RK4, 0.4, 1.0)
+def case(name, cells, variants, order=8, rk=ndgx.RK4):
+    dim = len(cells)
+    mesh = ndgx.Mesh(dim, cells, order)
+    model = ndgx.EquationModel.isothermal_euler(dim, 1.0)
+    cfg = ndgx.SolverConfig(mesh, model, rk, 0.4, 1.0)
     u0 = ndgx.init_euler_subsonic(mesh, model)
     with ndgx.Solver(cfg, arith=arith) as s:
         base, bst = timed(s, u0)
@@ -58,3 +59,8 @@ case("C3 768^2", (768, 768), [
 case("C5/8-sized blocks 2048x512", (2048, 512), [
     ("partitioned P=2 (2,1,1): two 1024x512 blocks", lambda c: ndgx.Solver.partitioned(c, 2, arith=arith)),
 ])
+if len(sys.argv) > 2 and sys.argv[2] == "3d":
+    # the C4 weak-scaling shape at N = 2: two 128^3 z-slabs (decompose -> (1, 1, 2))
+    case("C4 x2 128x128x256 (3D Euler o4 RK6)", (128, 128, 256), [
+        ("partitioned P=2 (1,1,2): two 128^3 z-slabs", lambda c: ndgx.Solver.partitioned(c, 2, arith=arith)),
+    ], order=4, rk=ndgx.RK6)
