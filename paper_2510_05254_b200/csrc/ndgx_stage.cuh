@@ -46,6 +46,9 @@ namespace ndgx {
 // many-term RK6 stages keep their face loads in flight (C4, 128^3: the 2..5
 // term stages 6.75 / 7.55 / 8.24 / 9.31 ms vs 8.51 / 9.14 / 9.87 / 11.53 ms in
 // the generic body).
+#ifndef NDGX_YTR2
+#define NDGX_YTR2 1  // flagship: y-face traces as one 16-byte store per variable
+#endif
 #ifndef NDGX_GEN_UTRACE
 #define NDGX_GEN_UTRACE 1  // generic body: face traces hold U only (flux and speed recomputed at the face)
 #endif
@@ -1065,12 +1068,23 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
 #pragma unroll
       for (int v = 0; v < NV; ++v) t[v * L] = U[v];
     }
+#if !NDGX_YTR2
     if (ln.r == 0 || ln.r == N - 1) {
       double* t = sT + ((ln.r == 0 ? 2 : 3) * HW) * L + i;
 #pragma unroll
       for (int v = 0; v < NV; ++v) t[v * L] = U[v];
     }
+#endif
   }
+#if NDGX_YTR2
+  // y-face traces of both nodes at once (i = 2c, 2c + 1 are adjacent slots):
+  // one 16-byte store per variable by the r = 0 / 7 lanes
+  if (ln.r == 0 || ln.r == N - 1) {
+    double* t = sT + ((ln.r == 0 ? 2 : 3) * HW) * L + 2 * ln.c;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) *reinterpret_cast<double2*>(t + v * L) = make_double2(Up[0][v], Up[1][v]);
+  }
+#endif
 #pragma unroll
   for (int v = 0; v < NV; ++v)
     *reinterpret_cast<double2*>(sF + v * NPE + ln.n0s) = make_double2(Fyp[0][v], Fyp[1][v]);
