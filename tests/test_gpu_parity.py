@@ -8,6 +8,8 @@ Bar (SURVEY.md §8c / north_star):
   after the fixed steps (tolerance written below as REL_L2_TOL);
 * integer work (layout permutation, decomposition): exact.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -275,3 +277,71 @@ def test_every_shape_matches_port(port, shape):
         else:
             assert max(rel_l2(port, p, r0, r_want)) <= REL_L2_TOL
             assert max(rel_l2(port, p, uf, want)) <= REL_L2_TOL
+
+
+def _ref_workers():
+    return max(1, min(16, os.cpu_count() or 1))
+
+
+def test_full_size_c3_five_steps_against_the_reference(reference):
+    """C3 at full size (768^2 cells, 1.13e8 DOF), 5 CFL steps against the
+    reference itself (its run_partitioned over the host's threads, whose
+    states equal its serial advance): exact bitwise, fast within REL_L2_TOL."""
+    p = Problem(2, (768, 768), 8, EULER, RK4)
+    mesh = ndgx.Mesh(2, (768, 768), 8)
+    u0 = ndgx.init_euler_subsonic(mesh, ndgx.EquationModel.isothermal_euler(2, 1.0))
+    want, st_w = reference.run_partitioned(p, u0, _ref_workers(), 5)
+    for arith in (ndgx.ARITH_EXACT, ndgx.ARITH_FAST):
+        with ndgx.Solver(config_of(p), arith=arith) as s:
+            s.upload(u0)
+            st = s.advance(ndgx.StepPlan(5, False))
+            got = s.download()
+        if arith == ndgx.ARITH_EXACT:
+            assert np.array_equal(got, want) and st.dt_min == st_w.dt_min and st.dt_max == st_w.dt_max
+        else:
+            d = got - want
+            for v in range(3):
+                assert np.sqrt((d[v::3] ** 2).sum() / (want[v::3] ** 2).sum()) <= REL_L2_TOL
+
+
+@pytest.mark.parametrize("n,steps", [(64, 5), (128, 3)], ids=["64cubed", "128cubed_full_size"])
+def test_3d_euler_rk6_against_the_reference(reference, n, steps):
+    """The C4 shape (3D isothermal Euler o4 RK6) at 64^3 cells (6.7e7 DOF, 5
+    steps) and at the benchmark size 128^3 (5.4e8 DOF, 3 steps) against the
+    reference: exact bitwise, fast within REL_L2_TOL (the line body, z-runs)."""
+    p = Problem(3, (n, n, n), 4, EULER, RK6)
+    cfg = config_of(p)
+    u0 = ndgx.init_euler_subsonic(cfg.mesh, cfg.model)
+    want, st_w = reference.run_partitioned(p, u0, _ref_workers(), steps)
+    for arith in (ndgx.ARITH_EXACT, ndgx.ARITH_FAST):
+        with ndgx.Solver(cfg, arith=arith) as s:
+            s.upload(u0)
+            st = s.advance(ndgx.StepPlan(steps, False))
+            got = s.download()
+        if arith == ndgx.ARITH_EXACT:
+            assert np.array_equal(got, want) and st.dt_max == st_w.dt_max
+        else:
+            d = got - want
+            for v in range(4):
+                den = (want[v::4] ** 2).sum()
+                assert np.sqrt((d[v::4] ** 2).sum() / den) <= REL_L2_TOL if den > 0 else np.abs(d[v::4]).max() <= 1e-13
+
+
+def test_full_size_c4_fast_equals_exact_and_conserves():
+    """C4 at the benchmark size (128^3 cells, 5.4e8 DOF), 3 steps: the fast
+    mode within REL_L2_TOL of the bit-identical mode, totals conserved."""
+    cfg = ndgx.SolverConfig(ndgx.Mesh(3, (128, 128, 128), 4), ndgx.EquationModel.isothermal_euler(3, 1.0), ndgx.RK6)
+    out = {}
+    for arith in (ndgx.ARITH_EXACT, ndgx.ARITH_FAST):
+        with ndgx.Solver(cfg, arith=arith) as s:
+            s.init_device(ndgx.IC_EULER_SUBSONIC)
+            t0 = s.conserved_totals_device()
+            s.advance(ndgx.StepPlan(3, False))
+            out[arith] = (s.download(), s.conserved_totals_device(), t0)
+    ue, uf = out[ndgx.ARITH_EXACT][0], out[ndgx.ARITH_FAST][0]
+    for v in range(4):
+        den = (ue[v::4] ** 2).sum()
+        d = np.sqrt(((ue[v::4] - uf[v::4]) ** 2).sum() / den) if den > 0 else np.abs(uf[v::4]).max()
+        assert d <= REL_L2_TOL
+    tot, t0 = out[ndgx.ARITH_FAST][1], out[ndgx.ARITH_FAST][2]
+    assert abs(tot[0] - t0[0]) <= 1e-12 * abs(t0[0])
