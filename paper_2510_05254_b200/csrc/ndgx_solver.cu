@@ -707,7 +707,14 @@ struct ndgx_solver {
       if (bk) {
         worker = bk->id;
         for (int x = 0; x < 3; ++x) lc[x] = g[x] - bk->goff[x];
-        const size_t idx = device_index(*bk, lc, node, 0);
+        // scan keys carry the AoS node; operator keys the reference's
+        // volume-traversal order (line (j, k) outer, i inner: j N + i in 2D,
+        // (j N + k) N + i in 3D) so that the earliest key is its first failure
+        int aos = node;
+        if (phase != ndgx::kPhaseScan && dim == 2) aos = (node % N) * N + node / N;
+        if (phase != ndgx::kPhaseScan && dim == 3)
+          aos = ((node % N) * N + node / (N * N)) * N + (node / N) % N;
+        const size_t idx = device_index(*bk, lc, aos, 0);
         code = NDGX_ERR_PHYSICS;
         if (phase == ndgx::kPhaseScan) {
           const double rho = fetch(*bk, u_buf(*bk, par), idx);

@@ -345,3 +345,25 @@ def test_full_size_c4_fast_equals_exact_and_conserves():
         assert d <= REL_L2_TOL
     tot, t0 = out[ndgx.ARITH_FAST][1], out[ndgx.ARITH_FAST][2]
     assert abs(tot[0] - t0[0]) <= 1e-12 * abs(t0[0])
+
+
+@pytest.mark.parametrize("dim,cells,order", [(3, (4, 3, 5), 4), (2, (6, 5), 8), (2, (7, 5), 4), (3, (3, 4, 2), 2)],
+                         ids=["3D-o4-lines", "2D-o8-flagship", "2D-o4-groups", "3D-o2-groups"])
+@pytest.mark.parametrize("arith", [ndgx.ARITH_EXACT, ndgx.ARITH_FAST], ids=["exact", "fast"])
+def test_operator_physics_error_names_the_cell_in_every_body(port, dim, cells, order, arith):
+    """A non-positive density at one node: serial_rhs's PhysicsError
+    (solver.cpp:258-261) names the same cell and value as the reference's,
+    from every stage-kernel body, in both arithmetic modes."""
+    p = Problem(dim, cells, order, EULER, RK4)
+    cfg = config_of(p)
+    u = ndgx.init_euler_subsonic(cfg.mesh, cfg.model)
+    nv = dim + 1
+    bad = (p.size // nv) // 2 + 1  # a node inside the mesh
+    u[bad * nv] = -0.5
+    with pytest.raises(Exception) as want:
+        port.rhs(p, u)
+    with ndgx.Solver(cfg, arith=arith) as s:
+        s.upload(u)
+        with pytest.raises(ndgx.PhysicsError) as got:
+            s.rhs()
+    assert str(got.value) == want.value.message
