@@ -334,6 +334,8 @@ def main(argv=None) -> int:
     ap.add_argument("--compare-equations", action="store_true")
     ap.add_argument("--arith", choices=["exact", "fast"], default="exact")
     ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--devices", type=int, action="append",
+                    help="GPUs of the multi-worker rows (block w on devices[w %% len]); default [--device]")
     ap.add_argument("--out", default=None, help="report path (default: <experiment>.csv)")
     a = ap.parse_args(argv)
     if a.equation == "advection" and a.seed is None:
@@ -342,7 +344,8 @@ def main(argv=None) -> int:
         ap.error("--cells is required (one value per run in the sweep)")
     spec = ExperimentSpec(a.experiment, a.equation, a.dim, a.order or [4], a.rk, a.cells, a.nk, a.seed or 0,
                           a.workers or [1], a.cfl, a.t_end, a.steps, compare_equations=a.compare_equations)
-    rep = run_experiment(spec, Runner(a.device, ndgx.ARITH_FAST if a.arith == "fast" else ndgx.ARITH_EXACT))
+    rep = run_experiment(spec, Runner(a.device, ndgx.ARITH_FAST if a.arith == "fast" else ndgx.ARITH_EXACT,
+                                      a.devices))
     from .report import report_to_csv
     with open(a.out or f"{a.experiment}.csv", "w") as f:
         f.write(report_to_csv(rep))
