@@ -369,8 +369,10 @@ def bench_ours(args):
     value = dof_total * stages * args.steps / t_dev
 
     # ---- per-stage timing inside the replayed step graph (globaltimer stamps) ----
-    stage_ms, ctl_ms = s.profile_step()
-    stage_ms = np.array(stage_ms)
+    # (median over 5 replays: a single replay varies by a few percent between runs)
+    profs = [s.profile_step() for _ in range(5)]
+    stage_ms = np.median(np.array([pr[0] for pr in profs]), axis=0)
+    ctl_ms = float(np.median([pr[1] for pr in profs]))
     avg_stage_ms = float(stage_ms.mean())
     bytes_per_launch = BYTES_PER_DOF_STAGE[rk] * dof
     peak, peak_src = measured_peaks()
@@ -506,7 +508,7 @@ def bench_ours(args):
                          "bytes_per_dof_stage": BYTES_PER_DOF_STAGE[rk],
                          "avg_launch_ms": avg_stage_ms, "stage_ms": stage_ms.tolist(), "step_control_ms": ctl_ms,
                          "stage_timing": "globaltimer stamps between the stages of the replayed two-step graph "
-                                         "(steady state, one extra 1-thread launch per stage)",
+                                         "(steady state, one extra 1-thread launch per stage), median of 5 replays",
                          "peak_source": peak_src,
                          "step_frac": value / world * BYTES_PER_DOF_STAGE[rk] / 1e9 / peak,
                          "sharded": sharded},
