@@ -83,7 +83,12 @@ struct Geo {
   static constexpr int THREADS = 32 * WARPS;
   static constexpr int MAXD = 4;                                      // max ring depth per warp
   static constexpr int RED = 2 * WARPS;                      // block reduction scratch (doubles)
-  static constexpr int HEAD = WARPS * MAXD + RED;            // 8-byte words before the slabs
+  // the generic body's operator rows K_d[k][.] in shared memory, rows padded
+  // to N + 1 doubles: lanes reading different rows k hit different banks (a
+  // per-lane index into the kernel parameters serialises in the constant cache)
+  static constexpr int KROW = N + 1;
+  static constexpr int KSM = ((DIM * N * KROW) + 1) & ~1;
+  static constexpr int HEAD = WARPS * MAXD + RED + KSM;      // 8-byte words before the slabs
   static constexpr int CHUNK = NV * NPE;                     // one array of one element (doubles)
   // generic body: lanes per element (GL) and elements per warp (EPW).  Small
   // elements share a warp so the node and face passes keep the lanes busy:
@@ -1287,6 +1292,15 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   if (lane == 0)
     for (int q = 0; q < depth; ++q) mbar_init(&bar[q], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // K rows for the generic body (one CTA barrier per launch, before any element)
+  double* const sK = smem + G::WARPS * G::MAXD + G::RED;
+  if constexpr (!USE_MMA && !USE_MMA3) {
+    for (int q = threadIdx.x; q < DIM * N * N; q += G::THREADS) {
+      const int d = q / (N * N), r = q - d * N * N;
+      sK[(d * N + r / N) * G::KROW + r % N] = p.K[d][r];
+    }
+    __syncthreads();
+  }
   __syncwarp();
   // lane 0 streams element ee's u and K_j into ring slot q with one bulk copy each
   // element ee = (ex, ey, ez): lane 0 streams its u and K_j into ring slot q
@@ -1584,7 +1598,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         for (int d = 0; d < DIM; ++d) {
           const int k = G::pos_of(d, n), t = G::line_of(d, n);
           const double* Fl = gF + (d * NV + v) * NPE;
-          const double* Kr = &p.K[d][k * N];
+          const double* Kr = sK + (d * N + k) * G::KROW;
           // 0 + K0 F0 + K1 F1 + ...: the leading 0 + only normalises a -0,
           // which zero_plus (axis 0) or the add onto dudt (axes > 0) reproduces
           double acc = A::mul(Kr[0], Fl[G::node(d, t, 0)]);
