@@ -46,6 +46,9 @@ namespace ndgx {
 // many-term RK6 stages keep their face loads in flight (C4, 128^3: the 2..5
 // term stages 6.75 / 7.55 / 8.24 / 9.31 ms vs 8.51 / 9.14 / 9.87 / 11.53 ms in
 // the generic body).
+#ifndef NDGX_GPF
+#define NDGX_GPF 1  // generic body: all of a lane's node loads issued before any combination
+#endif
 #ifndef NDGX_YTR2
 #define NDGX_YTR2 1  // flagship: y-face traces as one 16-byte store per variable
 #endif
@@ -1481,6 +1484,29 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     // ------------------------------------------------ 1: nodes
     // lane's nodes: n = sub + GL m
     double Sn[G::NMG][NV];  // last stage: S at the lane's nodes
+#if NDGX_GPF
+    // direct loads: every node's raw values first (one memory latency for
+    // all of the lane's nodes instead of one per node).  Measured
+    // (profiles/r02/generic_prefetch_ab.jsonl): the 2D order-8 exact body (the
+    // drop-in's default mode on C3) 8.95e10 -> 9.6e10; a loss for the other
+    // shapes (2D o4/o6 fast -5..-8%, 3D o4 exact -6%), which keep the plain loads
+    constexpr bool GPF = DIM == 2 && N == 8;
+    double rawn[G::NMG][NV][1 + NU];
+    if (GPF && depth == 0) {
+#pragma unroll
+      for (int m = 0; m < G::NMG; ++m) {
+        const int n = sub + GL * m;
+        if (!act || n >= NPE) continue;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const size_t g = ebase + (size_t)v * NPE + n;
+          rawn[m][v][0] = __ldg(p.u + g);
+#pragma unroll
+          for (int t = 0; t < NU; ++t) rawn[m][v][1 + t] = __ldg(p.ku[t] + g);
+        }
+      }
+    }
+#endif
 #pragma unroll
     for (int m = 0; m < G::NMG; ++m) {
       const int n = sub + GL * m;
@@ -1492,6 +1518,11 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         if (depth > 0)
           combine_s<EXACT, NU, AM, BM>(p, src + v * NPE + n, G::CHUNK, last, U[v], S);
         else
+#if NDGX_GPF
+        if (GPF)
+          combine_s<EXACT, NU, AM, BM>(p, rawn[m][v], 1, last, U[v], S);
+        else
+#endif
           combine_g<EXACT, NU, AM, BM>(p, ebase + (size_t)v * NPE + n, last, U[v], S);
         Sn[m][v] = S;
       }
