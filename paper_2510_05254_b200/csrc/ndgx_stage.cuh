@@ -46,6 +46,9 @@ namespace ndgx {
 // many-term RK6 stages keep their face loads in flight (C4, 128^3: the 2..5
 // term stages 6.75 / 7.55 / 8.24 / 9.31 ms vs 8.51 / 9.14 / 9.87 / 11.53 ms in
 // the generic body).
+#ifndef NDGX_LINE8
+#define NDGX_LINE8 1  // 2D order-8 exact body: volume sums by line tasks
+#endif
 #ifndef NDGX_GPF
 #define NDGX_GPF 1  // generic body: all of a lane's node loads issued before any combination
 #endif
@@ -1471,6 +1474,11 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   auto generic_element = [&](const int e, const int cx, const int cy, const int cz, const double* src,
                              const double* fsrc, const bool act) {
     constexpr int GL = G::GL;
+    // the 2D order-8 exact body sums its volume terms by line tasks (phase 3)
+    constexpr bool LINE8 = NDGX_LINE8 != 0 && EXACT && DIM == 2 && N == 8 && GL == 32;
+    // F_x / x-part slot of node (i, j): 8 j + (i ^ j) -- an x line read at a
+    // fixed position by 8 lanes (8 lines) covers 8 distinct banks
+    auto sx8 = [](int n) { return (n & ~7) | ((n ^ (n >> 3)) & 7); };
     const int sub = GL == 32 ? lane : (lane & (GL - 1)), grp = GL == 32 ? 0 : lane / GL;
     double* const gF = sF + grp * G::GSTRIDE;
     double* const gT = gF + G::OFF_T;
@@ -1538,7 +1546,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
         double F[NV], sp;
         flux<DIM, KIND, EXACT>(p, U, d, F, sp, rinv);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) gF[(d * NV + v) * NPE + n] = F[v];
+        for (int v = 0; v < NV; ++v) gF[(d * NV + v) * NPE + (LINE8 && d == 0 ? sx8(n) : n)] = F[v];
         const int k = G::pos_of(d, n);
         if (k == 0 || k == N - 1) {
           double* t = gT + ((2 * d + (k == 0 ? 0 : 1)) * G::TW) * L + G::line_of(d, n);
@@ -1617,6 +1625,47 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     __syncwarp();
 
     // ------------------------------------------------ 3: volume, faces, epilogue
+    // 2D order 8, exact: the volume sums by line tasks.  Lane = (axis d =
+    // lane / 16, line t, half): outputs k = 4 half .. 4 half + 3 of line t,
+    // every variable, each sum in the reference's order (one pass over the
+    // line's 8 fluxes instead of 8 slab reads per output and axis).  The x
+    // part (with its lifted faces) and the bare y sum go back into the flux
+    // slab; each node owner then finishes D = Dx + Sy + y lifts exactly as
+    // the per-node loop below does, so the states stay bit-identical.
+    if constexpr (LINE8) {
+      const int d = lane >> 4, t = (lane >> 1) & 7, half = lane & 1;
+      double fl[NV][N];
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int l = 0; l < N; ++l) fl[v][l] = gF[(d * NV + v) * NPE + (d == 0 ? sx8(l + 8 * t) : t + 8 * l)];
+      double res[4][NV];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = 4 * half + kk;
+        const double* Kr = sK + (d * N + k) * G::KROW;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double acc = A::mul(Kr[0], fl[v][0]);
+#pragma unroll
+          for (int l = 1; l < N; ++l) acc = A::mac(acc, Kr[l], fl[v][l]);
+          if (d == 0) {
+            acc = zero_plus(acc);
+            if (k == 0) acc = A::add(acc, A::mul(p.lift[0], gH[(0 * NV + v) * L + t]));
+            if (k == N - 1) acc = A::sub(acc, A::mul(p.lift[0], gH[(1 * NV + v) * L + t]));
+          }
+          res[kk][v] = acc;
+        }
+      }
+      __syncwarp();  // every line's flux reads precede the in-place stores
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = 4 * half + kk;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) gF[(d * NV + v) * NPE + (d == 0 ? sx8(k + 8 * t) : t + 8 * k)] = res[kk][v];
+      }
+      __syncwarp();
+    }
 #pragma unroll
     for (int m = 0; m < G::NMG; ++m) {
       const int n = sub + GL * m;
@@ -1625,8 +1674,14 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         double D = 0.0;
+        if constexpr (LINE8) {
+          const int i = n & 7, j = n >> 3;
+          D = A::add(gF[v * NPE + sx8(n)], gF[(NV + v) * NPE + n]);
+          if (j == 0) D = A::add(D, A::mul(p.lift[1], gH[(2 * NV + v) * L + i]));
+          if (j == N - 1) D = A::sub(D, A::mul(p.lift[1], gH[(3 * NV + v) * L + i]));
+        }
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) {
+        for (int d = 0; d < (LINE8 ? 0 : DIM); ++d) {
           const int k = G::pos_of(d, n), t = G::line_of(d, n);
           const double* Fl = gF + (d * NV + v) * NPE;
           const double* Kr = sK + (d * N + k) * G::KROW;
