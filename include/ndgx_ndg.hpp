@@ -14,7 +14,7 @@
 //
 // Arithmetic: every entry takes `arith` last.  The default NDGX_ARITH_EXACT
 // is bit-identical to the reference (the reference's unfused operation
-// order: 8.1e10 DOF*stage/s on C3).  NDGX_ARITH_FAST (FMA contraction, FP64
+// order: 1.02e11 DOF*stage/s on C3).  NDGX_ARITH_FAST (FMA contraction, FP64
 // tensor cores; <= 1e-12 relative L2 vs the reference) is the headline
 // throughput, 1.96e11 -- pass it explicitly.
 //
