@@ -46,6 +46,9 @@ namespace ndgx {
 // many-term RK6 stages keep their face loads in flight (C4, 128^3: the 2..5
 // term stages 6.75 / 7.55 / 8.24 / 9.31 ms vs 8.51 / 9.14 / 9.87 / 11.53 ms in
 // the generic body).
+#ifndef NDGX_LINEG
+#define NDGX_LINEG 1  // generic 2D bodies: volume sums by whole-line tasks
+#endif
 #ifndef NDGX_LINE8
 #define NDGX_LINE8 1  // 2D order-8 exact body: volume sums by line tasks
 #endif
@@ -1476,6 +1479,11 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     constexpr int GL = G::GL;
     // the 2D order-8 exact body sums its volume terms by line tasks (phase 3)
     constexpr bool LINE8 = NDGX_LINE8 != 0 && EXACT && DIM == 2 && N == 8 && GL == 32;
+    // 2D orders 6-7 (and odd-order advection) sum by whole-line tasks
+    // (NDGX_LINEG; profiles/r02/lineg_ab.jsonl: 2D Euler o6 8.1e10 -> 8.6e10,
+    // advection o6 9.1e10 -> 1.0e11, o7 5.3e10 -> 6.2e10; a loss for o2/o4 and
+    // for Euler o3/o5, which keep the per-node sums)
+    constexpr bool LINEG = NDGX_LINEG != 0 && !LINE8 && DIM == 2 && (N >= 6 || (KIND == 0 && (N & 1) != 0));
     // F_x / x-part slot of node (i, j): 8 j + (i ^ j) -- an x line read at a
     // fixed position by 8 lanes (8 lines) covers 8 distinct banks
     auto sx8 = [](int n) { return (n & ~7) | ((n ^ (n >> 3)) & 7); };
@@ -1632,6 +1640,41 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     // part (with its lifted faces) and the bare y sum go back into the flux
     // slab; each node owner then finishes D = Dx + Sy + y lifts exactly as
     // the per-node loop below does, so the states stay bit-identical.
+    if constexpr (LINEG) {
+      // general 2D shapes: whole lines, task q = sub + GL r (x lines t = q,
+      // y lines t = q - N); each F slot is read only by its own line's task,
+      // so the parts go back in place as they are formed
+#pragma unroll
+      for (int q0 = 0; q0 < 2 * N; q0 += GL) {
+        const int q = q0 + sub;
+        if (act && q < 2 * N) {
+          const int d = q >= N ? 1 : 0, t = q - d * N;
+          double* Fd = gF + d * NV * NPE;
+          double fl[NV][N];
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int l = 0; l < N; ++l) fl[v][l] = Fd[v * NPE + (d == 0 ? l + N * t : t + N * l)];
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            const double* Kr = sK + (d * N + k) * G::KROW;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              double acc = A::mul(Kr[0], fl[v][0]);
+#pragma unroll
+              for (int l = 1; l < N; ++l) acc = A::mac(acc, Kr[l], fl[v][l]);
+              if (d == 0) {
+                acc = zero_plus(acc);
+                if (k == 0) acc = A::add(acc, A::mul(p.lift[0], gH[(0 * NV + v) * L + t]));
+                if (k == N - 1) acc = A::sub(acc, A::mul(p.lift[0], gH[(1 * NV + v) * L + t]));
+              }
+              Fd[v * NPE + (d == 0 ? k + N * t : t + N * k)] = acc;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
     if constexpr (LINE8) {
       const int d = lane >> 4, t = (lane >> 1) & 7, half = lane & 1;
       double fl[NV][N];
@@ -1674,14 +1717,14 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         double D = 0.0;
-        if constexpr (LINE8) {
-          const int i = n & 7, j = n >> 3;
-          D = A::add(gF[v * NPE + sx8(n)], gF[(NV + v) * NPE + n]);
+        if constexpr (LINE8 || LINEG) {
+          const int i = n % N, j = n / N;
+          D = A::add(gF[v * NPE + (LINE8 ? sx8(n) : n)], gF[(NV + v) * NPE + n]);
           if (j == 0) D = A::add(D, A::mul(p.lift[1], gH[(2 * NV + v) * L + i]));
           if (j == N - 1) D = A::sub(D, A::mul(p.lift[1], gH[(3 * NV + v) * L + i]));
         }
 #pragma unroll
-        for (int d = 0; d < (LINE8 ? 0 : DIM); ++d) {
+        for (int d = 0; d < (LINE8 || LINEG ? 0 : DIM); ++d) {
           const int k = G::pos_of(d, n), t = G::line_of(d, n);
           const double* Fl = gF + (d * NV + v) * NPE;
           const double* Kr = sK + (d * N + k) * G::KROW;
