@@ -17,6 +17,12 @@ CASES = [
     ("2D Euler o4 fast (8 lanes per element)", 2, (9, 7), 4, True, ndgx.RK3, ndgx.ARITH_FAST, None),
     ("1D advection o3 exact (4 lanes per element, ring)", 1, (33,), 3, False, ndgx.RK4, ndgx.ARITH_EXACT, None),
     ("3D advection o2 (8 lanes per element)", 3, (3, 4, 5), 2, False, ndgx.RK4, ndgx.ARITH_FAST, None),
+    ("3D Euler o4 RK6 fast, 16 z planes (line body, z-runs of 8)", 3, (3, 2, 16), 4, True, ndgx.RK6,
+     ndgx.ARITH_FAST, None),
+    ("2D Euler o8 exact (line-task volume)", 2, (5, 4), 8, True, ndgx.RK4, ndgx.ARITH_EXACT, None),
+    ("2D Euler o6 fast (whole-line volume, 8 lanes per element)", 2, (7, 5), 6, True, ndgx.RK4, ndgx.ARITH_FAST,
+     None),
+    ("2D advection o7 exact (whole-line volume)", 2, (4, 3), 7, False, ndgx.RK3, ndgx.ARITH_EXACT, None),
 ]
 for name, dim, cells, order, euler, rk, arith, depth in CASES:
     if depth is None:
