@@ -1483,7 +1483,12 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     // (NDGX_LINEG; profiles/r02/lineg_ab.jsonl: 2D Euler o6 8.1e10 -> 8.6e10,
     // advection o6 9.1e10 -> 1.0e11, o7 5.3e10 -> 6.2e10; a loss for o2/o4 and
     // for Euler o3/o5, which keep the per-node sums)
-    constexpr bool LINEG = NDGX_LINEG != 0 && !LINE8 && DIM == 2 && (N >= 6 || (KIND == 0 && (N & 1) != 0));
+#ifndef NDGX_LINEG3
+#define NDGX_LINEG3 0x1C0  // 3D orders (bit N) taking the whole-line volume: 6-8 (o6 1.7e10 -> 2.0e10; o3 and exact o4 lose 15-19%)
+#endif
+    constexpr bool LINEG = NDGX_LINEG != 0 && !LINE8 &&
+                           ((DIM == 2 && (N >= 6 || (KIND == 0 && (N & 1) != 0))) ||
+                            (DIM == 3 && ((NDGX_LINEG3 >> N) & 1) != 0));
     // F_x / x-part slot of node (i, j): 8 j + (i ^ j) -- an x line read at a
     // fixed position by 8 lanes (8 lines) covers 8 distinct banks
     auto sx8 = [](int n) { return (n & ~7) | ((n ^ (n >> 3)) & 7); };
@@ -1645,16 +1650,16 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       // y lines t = q - N); each F slot is read only by its own line's task,
       // so the parts go back in place as they are formed
 #pragma unroll
-      for (int q0 = 0; q0 < 2 * N; q0 += GL) {
+      for (int q0 = 0; q0 < DIM * L; q0 += GL) {
         const int q = q0 + sub;
-        if (act && q < 2 * N) {
-          const int d = q >= N ? 1 : 0, t = q - d * N;
+        if (act && q < DIM * L) {
+          const int d = q / L, t = q - d * L;
           double* Fd = gF + d * NV * NPE;
           double fl[NV][N];
 #pragma unroll
           for (int v = 0; v < NV; ++v)
 #pragma unroll
-            for (int l = 0; l < N; ++l) fl[v][l] = Fd[v * NPE + (d == 0 ? l + N * t : t + N * l)];
+            for (int l = 0; l < N; ++l) fl[v][l] = Fd[v * NPE + G::node(d, t, l)];
 #pragma unroll
           for (int k = 0; k < N; ++k) {
             const double* Kr = sK + (d * N + k) * G::KROW;
@@ -1668,7 +1673,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
                 if (k == 0) acc = A::add(acc, A::mul(p.lift[0], gH[(0 * NV + v) * L + t]));
                 if (k == N - 1) acc = A::sub(acc, A::mul(p.lift[0], gH[(1 * NV + v) * L + t]));
               }
-              Fd[v * NPE + (d == 0 ? k + N * t : t + N * k)] = acc;
+              Fd[v * NPE + G::node(d, t, k)] = acc;
             }
           }
         }
@@ -1718,10 +1723,15 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       for (int v = 0; v < NV; ++v) {
         double D = 0.0;
         if constexpr (LINE8 || LINEG) {
-          const int i = n % N, j = n / N;
-          D = A::add(gF[v * NPE + (LINE8 ? sx8(n) : n)], gF[(NV + v) * NPE + n]);
-          if (j == 0) D = A::add(D, A::mul(p.lift[1], gH[(2 * NV + v) * L + i]));
-          if (j == N - 1) D = A::sub(D, A::mul(p.lift[1], gH[(3 * NV + v) * L + i]));
+          // D = x part (with x lifts), then per further axis: + its sum, its lifts
+          D = gF[v * NPE + (LINE8 ? sx8(n) : n)];
+#pragma unroll
+          for (int d = 1; d < DIM; ++d) {
+            const int k = G::pos_of(d, n), t = G::line_of(d, n);
+            D = A::add(D, gF[(d * NV + v) * NPE + n]);
+            if (k == 0) D = A::add(D, A::mul(p.lift[d], gH[((2 * d) * NV + v) * L + t]));
+            if (k == N - 1) D = A::sub(D, A::mul(p.lift[d], gH[((2 * d + 1) * NV + v) * L + t]));
+          }
         }
 #pragma unroll
         for (int d = 0; d < (LINE8 || LINEG ? 0 : DIM); ++d) {
