@@ -1422,7 +1422,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   int slot = 0;
   uint32_t parity = 0;
 #ifndef NDGX_XRUN
-#define NDGX_XRUN 4
+#define NDGX_XRUN 2  // run length (C3 2.228 vs 2.246 ms/step at 4, 2.284 at 8; C5 18.32 vs 18.46 at 4)
 #endif
   // (measured per stage: a win for the Euler last stage, 0.96 -> 0.83 ms on
   // C3, whose x-lo reuse saves two arrays' face loads; a loss elsewhere)
