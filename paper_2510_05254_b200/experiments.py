@@ -303,12 +303,100 @@ def run_timing(spec: ExperimentSpec, runner: Optional[Runner] = None) -> BenchRe
     return report
 
 
+def weak_grid(dim: int, cells: int, p: int) -> Tuple[int, int, int]:
+    """run_scale's weak-scaling factorisation (src/experiments.cpp:352-378): the
+    lowest-interface (px, py, pz) of p workers for c cells per worker per axis,
+    ties broken by the lexicographically smallest grid."""
+    best, best_cost = (1, 1, 1), -1
+    for px in range(1, p + 1):
+        if p % px:
+            continue
+        rest = p // px
+        for py in range(1, rest + 1):
+            if rest % py:
+                continue
+            pz = rest // py
+            if dim < 3 and pz != 1:
+                continue
+            if dim < 2 and py != 1:
+                continue
+            grid = (px, py, pz)
+            cost = 0
+            for d in range(dim):
+                cross = 1
+                for e in range(dim):
+                    if e != d:
+                        cross *= cells * grid[e]
+                cost += grid[d] * cross
+            if best_cost < 0 or cost < best_cost or (cost == best_cost and grid < best):
+                best, best_cost = grid, cost
+    return best
+
+
+def run_scale(spec: ExperimentSpec, runner: Optional[Runner] = None) -> BenchReport:
+    """run_scale (src/experiments.cpp:306-399): per cell count, strong scaling
+    of the fixed grid against its 1-worker wall time, then weak scaling on the
+    lowest-interface grid of c cells per worker per axis against the 1-worker
+    time per DOF.  Multi-worker rows run through the partitioned handle
+    (Runner.devices: block w on devices[w % len]); on one GPU every block
+    shares it, so the speedup column measures the decomposition's cost there,
+    not a multi-GPU speedup (bench.py under torchrun gives those)."""
+    runner = runner or Runner()
+    report = new_report(spec)
+    if not spec.cells:
+        raise ndgx.ConfigError("empty cell sweep")
+    if spec.dim < 2:
+        raise ndgx.ConfigError("scaling runs need dim >= 2")
+    if spec.dim_compare:
+        raise ndgx.ConfigError("--dim-compare is not on the GPU path (SURVEY.md §8)")
+    order = spec.orders[0]
+
+    def run_one(mesh, workers, mode, baseline_wall, baseline_tpd):
+        model = spec_model(spec, spec.dim)
+        row = base_row(spec, mesh, model, workers)
+        row.note = mode
+        try:
+            initial = spec_initial(spec, mesh, model)
+            config = ndgx.SolverConfig(mesh, model, ndgx.rk_from_name(spec.rk), spec.cfl, spec.t_end)
+            _, stats = runner.timed_run(config, initial, ndgx.StepPlan(spec.steps, True), workers)
+            fill_stats(row, stats)
+            if baseline_wall > 0.0:
+                row.speedup = baseline_wall / stats.wall_seconds
+                row.efficiency = row.speedup / workers
+            if baseline_tpd > 0.0:
+                row.efficiency = baseline_tpd / row.time_per_dof
+        except ndgx.DecompositionError as e:
+            row.status = "skipped"
+            row.note = f"{mode}: {e}"
+        except RuntimeError as e:
+            row.status = "failed"
+            row.note = f"{mode}: {e}"
+        report.rows.append(row)
+        return row
+
+    for c in spec.cells:
+        glob = spec_mesh(spec.dim, c, order)
+        serial = run_one(glob, 1, "strong", 0.0, 0.0)
+        for p in spec.workers:
+            if p <= 1:
+                continue
+            run_one(glob, p, "strong", serial.wall_seconds if serial.status == "ok" else 0.0, 0.0)
+        weak_tpd = 0.0
+        for p in spec.workers:
+            g = weak_grid(spec.dim, c, p)
+            cells = tuple(c * g[a] for a in range(spec.dim))
+            row = run_one(ndgx.Mesh(spec.dim, cells, order), p, "weak", 0.0, weak_tpd)
+            if p == 1 and row.status == "ok":
+                weak_tpd = row.time_per_dof
+    return report
+
+
 def run_experiment(spec: ExperimentSpec, runner: Optional[Runner] = None) -> BenchReport:
     """run_experiment (src/experiments.cpp:521-531) for the sweeps on the GPU path."""
-    fns = {"converge": run_converge, "cost": run_cost, "fit": run_fit, "timing": run_timing}
+    fns = {"converge": run_converge, "cost": run_cost, "fit": run_fit, "timing": run_timing, "scale": run_scale}
     if spec.experiment not in fns:
         raise ndgx.ConfigError(f"unknown experiment '{spec.experiment}'"
-                               if spec.experiment not in ("scale", "energy", "simulate") else
+                               if spec.experiment not in ("energy", "simulate") else
                                f"experiment '{spec.experiment}' is not on the GPU path (SURVEY.md §8)")
     return fns[spec.experiment](spec, runner)
 
@@ -319,7 +407,7 @@ def main(argv=None) -> int:
     for the experiments on the GPU path; CSV reports only."""
     import argparse
     ap = argparse.ArgumentParser(prog="python -m paper_2510_05254_b200.experiments")
-    ap.add_argument("experiment", choices=["converge", "cost", "fit", "timing"])
+    ap.add_argument("experiment", choices=["converge", "cost", "fit", "timing", "scale"])
     ap.add_argument("--equation", default="advection")
     ap.add_argument("--dim", type=int, default=1)
     ap.add_argument("--order", type=int, action="append")

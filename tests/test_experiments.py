@@ -23,7 +23,7 @@ from paper_2510_05254_b200 import experiments as ex
 from paper_2510_05254_b200 import report as rp
 
 REF_EXP = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "_build", "ref_experiments")
-TIMING_COLS = {"wall_seconds", "time_per_dof"}
+TIMING_COLS = {"wall_seconds", "time_per_dof", "speedup", "efficiency"}  # measured, not computed from states
 
 
 def _ref_csv(spec: ex.ExperimentSpec) -> str:
@@ -58,6 +58,10 @@ SPECS = [
     ex.ExperimentSpec("fit", "advection", 1, [3, 5], "rk4", [8, 16, 32, 64], 7, 3),
     ex.ExperimentSpec("converge", "advection", 2, [4], "rk3", [4, 8], 3, 11, cfl=0.3, t_end=0.5),
     ex.ExperimentSpec("timing", "euler", 2, [8], "rk4", [6, 8], steps=12, compare_equations=True),
+    # run_scale: strong rows of an 8^2 grid at 1/2/4 workers, weak rows on the
+    # lowest-interface grids (multi-worker rows through the partitioned handle)
+    ex.ExperimentSpec("scale", "euler", 2, [4], "rk4", [8], workers=[1, 2, 4], steps=5),
+    ex.ExperimentSpec("scale", "advection", 3, [3], "rk3", [4], 3, 5, workers=[1, 3], steps=4),
 ]
 
 
@@ -119,9 +123,22 @@ def test_multi_worker_timing_rows_skip_undecomposable_meshes():
     assert [r.status for r in rows] == ["skipped"] and rows[0].workers == 3
 
 
-def test_scale_driver_is_not_on_the_gpu_path():
-    with pytest.raises(ndgx.ConfigError, match="not on the GPU path"):
-        ex.run_experiment(ex.ExperimentSpec("scale"))
+def test_energy_and_simulate_drivers_are_not_on_the_gpu_path():
+    for name in ("energy", "simulate"):
+        with pytest.raises(ndgx.ConfigError, match="not on the GPU path"):
+            ex.run_experiment(ex.ExperimentSpec(name))
+
+
+def test_weak_grid_is_the_references_lowest_interface_factorisation():
+    # src/experiments.cpp:352-378: ties go to the lexicographically smallest grid
+    assert ex.weak_grid(2, 8, 1) == (1, 1, 1)
+    assert ex.weak_grid(2, 8, 2) == (1, 2, 1)
+    assert ex.weak_grid(2, 8, 4) == (1, 4, 1)
+    assert ex.weak_grid(2, 8, 6) == (1, 6, 1)
+    assert ex.weak_grid(3, 4, 8) == (1, 1, 8)
+    assert ex.weak_grid(3, 4, 3) == (1, 1, 3)
+    with pytest.raises(ndgx.ConfigError, match="scaling runs need dim >= 2"):
+        ex.run_scale(ex.ExperimentSpec("scale", "advection", 1, [3], "rk3", [4], 3, 5))
 
 
 @pytest.mark.gpu
