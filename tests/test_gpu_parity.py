@@ -367,3 +367,27 @@ def test_operator_physics_error_names_the_cell_in_every_body(port, dim, cells, o
         with pytest.raises(ndgx.PhysicsError) as got:
             s.rhs()
     assert str(got.value) == want.value.message
+
+
+@pytest.mark.parametrize("dim,cells,order,kind", [
+    (2, (1, 3), 8, EULER), (2, (2, 1), 8, EULER), (2, (1, 1), 8, ADVECTION), (2, (3, 1), 4, EULER),
+    (3, (1, 1, 5), 4, EULER), (3, (2, 1, 1), 4, EULER), (3, (1, 2, 1), 4, ADVECTION), (1, (1,), 5, ADVECTION),
+], ids=lambda x: str(x).replace(" ", ""))
+def test_degenerate_meshes_match_port(port, dim, cells, order, kind):
+    """One-cell axes: the element is its own periodic neighbour (and runs,
+    lane groups and z-runs degenerate to length 1); exact bitwise, fast
+    within REL_L2_TOL."""
+    p = Problem(dim, cells, order, kind, RK4 if dim < 3 else RK6, velocity=(1.0, 0.5, -0.25))
+    cfg = config_of(p)
+    u0 = (ndgx.init_euler_subsonic(cfg.mesh, cfg.model) if kind == EULER
+          else ndgx.init_multisine(cfg.mesh, cfg.model, n_modes=2, seed=9))
+    want, _ = port.advance(p, u0, 3)
+    for arith in (ndgx.ARITH_EXACT, ndgx.ARITH_FAST):
+        with ndgx.Solver(cfg, arith=arith) as s:
+            s.upload(u0)
+            s.advance(ndgx.StepPlan(3, False))
+            got = s.download()
+        if arith == ndgx.ARITH_EXACT:
+            assert np.array_equal(got, want)
+        else:
+            assert max(rel_l2(port, p, got, want)) <= REL_L2_TOL
