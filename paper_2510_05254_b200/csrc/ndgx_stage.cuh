@@ -9,34 +9,35 @@
 //   CFL alpha        src/solver.cpp:310-334         fused into the last stage's epilogue
 //   finite check     src/solver.cpp:361-368
 //
-// Execution model: ONE ELEMENT PER WARP.  Every warp of a persistent grid
-// walks elements e = warp_id, warp_id + total_warps, ... (x fastest, so
-// neighbouring warps work on neighbouring elements and face-neighbour reads
-// hit L2) and runs, warp-locally with only __syncwarp between the steps:
+// Execution model: a persistent grid of warps, no CTA barriers during the
+// element work (__syncwarp only).  By default one element per warp; elements
+// are walked x fastest so neighbouring warps work on neighbouring elements
+// and face-neighbour reads hit L2.  Per element, warp-locally:
 //   1  node phase: each lane forms the stage input U_s = u + sum a K at its
-//      nodes straight from HBM (all of a lane's loads in flight together),
-//      the flux along every axis and the one-sided speeds; fluxes go to a
-//      warp-private shared-memory slab, face nodes also to a trace slab
-//   2  face phase: one lane per face node loads the neighbour element's face
-//      node (or the received multi-block plane), forms its stage input, flux
-//      and speed, and the Lax-Friedrichs flux of every variable
-//   3  output phase: the volume quadrature of every axis, the lifted face
-//      fluxes and the RK epilogue (K_s = dt*dudt, or u_new = S + b_s K_s,
-//      finite check, next-step wavespeed), stored straight to HBM.
-// No block barriers, no producer warps: latency is hidden by the many
-// independent warps per SM, and HBM traffic is the compulsory one array pass
-// per input and output (neighbour face nodes are L2 hits).
+//      nodes straight from HBM (all of a lane's loads in flight together);
+//   2  face phase: the Lax-Friedrichs flux at every face node, the
+//      neighbour's stage input from HBM (or the received multi-block plane);
+//   3  output phase: the volume quadrature, the lifted face fluxes and the
+//      RK epilogue (K_s = dt*dudt, or u_new = S + b_s K_s, finite check,
+//      next-step wavespeed), stored straight to HBM.
+// HBM traffic is the compulsory one array pass per input and output.
 //
-// Two volume back-ends:
-//   EXACT     the reference's operation order with _rn intrinsics (bit-
-//             identical states): per output node and axis, 0 + K0 F0 + ...,
-//             added once, faces after each axis.
-//   FAST, 2D N=8 (the flagship)  FP64 tensor cores, mma.sync.m8n8k4.f64: with
-//             lane = 4r + c the lane evaluates fluxes at nodes (i=c+4h, j=r),
-//             which are exactly its B fragments of D_x = K_x F_x; one
-//             warp-local transpose gives the A fragments of D_y = F_y K_y^T,
-//             accumulated onto D_x, and both land on nodes (i=r, j=2c+s).
-//   FAST, other shapes: the exact loop structure with contracted FMAs.
+// Bodies:
+//   2D N=8, FAST (the flagship, element_2d8_fast): FP64 tensor cores,
+//             mma.sync.m8n8k4.f64 -- lane = 4r + c evaluates fluxes at nodes
+//             (i = 2c + h, j = r), exactly its B fragments of D_x = K_x F_x; one
+//             warp-local transpose gives the A fragments of D_y = F_y K_y^T.
+//             Runs of 2 x-adjacent elements per warp (u-only and last stages)
+//             take the x-lo neighbour from the previous element's slab.
+//   3D N=4, FAST (element_3d4_lines): lanes own whole x / y / z lines of a
+//             swizzled U slab (conflict-free along every axis); z-runs per
+//             warp carry the z-hi face flux to the next element.
+//   generic (every other shape, and EXACT everywhere): the reference's loop
+//             structure; EXACT in its operation order with _rn intrinsics
+//             (bit-identical), FAST with contracted FMAs.  Small elements run
+//             G::EPW to a warp (G::GL lanes each); 2D orders 6-8 (and 3D 6-8)
+//             sum the volume by whole-line tasks, the 2D order-8 exact body
+//             by half-line tasks.
 #pragma once
 
 namespace ndgx {
