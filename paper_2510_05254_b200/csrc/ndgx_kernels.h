@@ -52,7 +52,7 @@ StageKernel make_stage_kernel() {
     k.fnx[8] = &stage_kernel<DIM, N, KIND, EXACT, 8, true>;
   }
   k.threads = G::THREADS;
-  k.warps = G::WARPS * G::EPW;
+  k.warps = G::WARPS * (G::mma_body(EXACT, 0) ? 1 : G::EPW);  // (the tensor-core bodies: one element per warp)
   for (int q = 0; q < kNumSigs; ++q)
     k.smem_fixed[q] = G::smem_bytes(0, 0, G::mma_body(EXACT, q), kSigs[q].bm != 0);
   k.ring_per_array = G::WARPS * G::SLOT1 * 8;

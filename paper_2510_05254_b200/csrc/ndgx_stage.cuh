@@ -29,6 +29,8 @@
 //             warp-local transpose gives the A fragments of D_y = F_y K_y^T.
 //             Runs of 2 x-adjacent elements per warp (u-only and last stages)
 //             take the x-lo neighbour from the previous element's slab.
+//             2D Euler N = 5..7 and advection N = 7 run it zero-padded to the
+//             8 x 8 grid (NDGX_MMA2_ORDERS[_ADV]).
 //   3D N=4, FAST (element_3d4_lines): lanes own whole x / y / z lines of a
 //             swizzled U slab (conflict-free along every axis); z-runs per
 //             warp carry the z-hi face flux to the next element.
@@ -67,6 +69,17 @@ namespace ndgx {
 #endif
 #ifndef NDGX_MMA3_SIGS
 #define NDGX_MMA3_SIGS 0x1FF
+#endif
+// bit N: the contracted 2D order-N (N < 8) stages run the flagship body
+// zero-padded to 8 x 8 nodes.  Measured at 1e8 DOF against the generic body
+// (profiles/r02/padded_mma_orders.jsonl): Euler o5 / o6 / o7 7.6 / 8.5 /
+// 7.1e10 -> 8.1e10 / 1.19e11 / 1.40e11; advection o7 6.0e10 -> 1.30e11,
+// o5 even, o6 1.02e11 -> 8.1e10 (its 4-lane groups win there)
+#ifndef NDGX_MMA2_ORDERS
+#define NDGX_MMA2_ORDERS 0x0E0  // Euler
+#endif
+#ifndef NDGX_MMA2_ORDERS_ADV
+#define NDGX_MMA2_ORDERS_ADV 0x080  // advection
 #endif
 
 template <int DIM, int N, int KIND>
@@ -132,7 +145,10 @@ struct Geo {
 #ifdef NDGX_NO_MMA  // A/B builds: the contracted generic (scalar DFMA) body instead of the tensor-core bodies
   static constexpr bool MMA = false, MMA3 = false;
 #else
-  static constexpr bool MMA = (DIM == 2 && N == 8);          // FAST-mode tensor-core volume (2D)
+  // FAST-mode tensor-core volume (2D): order 8, and the orders in
+  // NDGX_MMA2_ORDERS zero-padded to the 8 x 8 node grid of the same body
+  static constexpr bool MMA =
+      (DIM == 2 && (N == 8 || (N >= 5 && (((KIND == 1 ? NDGX_MMA2_ORDERS : NDGX_MMA2_ORDERS_ADV) >> N) & 1) != 0)));
   static constexpr bool MMA3 = (DIM == 3 && N == 4);         // FAST-mode tensor-core volume (3D)
 #endif
   // one face node per lane: the ring slot also carries the element's face
@@ -145,7 +161,7 @@ struct Geo {
   static constexpr __host__ __device__ int wslab(bool mma, bool last) {
     return mma ? (MMA3 ? (NDGX_LINES3 ? (4 + (last ? 1 : 0)) * NV * NPE  // line body: U | three dudt parts | S
                                       : (((3 + (last ? 1 : 0)) * NV * NPE + FACES * (NV + 1) * L + FACES * NV * L + 1) & ~1))
-                       : (((1 + (last ? 1 : 0)) * NV * NPE + FACES * HW * L + FACES * NV * L + 1) & ~1))
+                       : (((1 + (last ? 1 : 0)) * NV * 64 + FACES * HW * 8 + FACES * NV * 8 + 1) & ~1))
                : EPW * GSTRIDE;
   }
   // which body a (arith, signature) kernel runs: the 2D N=8 / 3D N=4
@@ -964,6 +980,13 @@ struct Lane8 {
   int xf;                // x face (0 / 1) feeding the output row r
   double kx[2], ky[2];   // K_x[r][2c+h], K_y[r][2c+h] (k-step h pairs l = 2c + h)
   int n0s, a0s, a1s;     // swizzled slab slots of n0 and of the A / output nodes o0, o0 + 8
+  // order N < 8 on the padded 8 x 8 grid (slab slots keep the padded index
+  // i + 8 j; padded nodes carry zero fluxes, padded K rows / columns are 0)
+  int g0;                // global node of the flux node (2c, r): i + N j
+  int og0, og1;          // global nodes of the output nodes (r, 2c), (r, 2c + 1)
+  int vm;                // valid bits: 1, 2 flux nodes h = 0, 1; 4, 8 output nodes s = 0, 1; 16 face node t
+  int yf0, yf1;          // y face (2 lo / 3 hi) lifted into output s = 0 / 1
+  double yco1p;          // its coefficient for s = 1 (yco0 for s = 0)
 };
 
 // Slab slot of node n = i + 8 j for the flagship's F_y and S arrays: the
@@ -973,12 +996,15 @@ struct Lane8 {
 // per half-warp instead of two (a 4-way conflict unswizzled).
 __host__ __device__ constexpr int swz8(int n) { return n ^ (((n >> 4) & 3) << 2); }
 
-template <int KIND, int NU, int AM, int BM, int SIG>
+template <int N, int KIND, int NU, int AM, int BM, int SIG>
 __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8& ln, int lane, int e, int cx,
-                                                 int cy, const double* src, const double* fsrc, bool ring,
+                                                 int cy, const double* src, const double* fsrc, bool ring_,
                                                  double* sF, double* sT, double* sH, double dt, bool last,
                                                  long long step, double& alpha, bool reuse_lo = false) {
-  constexpr int N = 8, NPE = 64, L = 8;
+  // N < 8: the same body on the zero-padded 8 x 8 grid (slab index i + 8 j)
+  constexpr bool PAD = N < 8;
+  constexpr int NPE = N * N, L = 8;
+  const bool ring = !PAD && ring_;  // (no TMA ring: odd or unaligned element chunks)
   constexpr int NV = KIND == 0 ? 1 : 3;
   constexpr int HW = 2 * NV + 1;
   constexpr int CHUNK = NV * NPE;
@@ -1008,7 +1034,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
     if (from_ext) {
       const size_t xs = d == 0 ? (size_t)cy : (size_t)cx;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) Nraw[0][v] = __ldg(ext + (xs * NV + v) * L + ln.t);
+      for (int v = 0; v < NV; ++v) Nraw[0][v] = __ldg(ext + (xs * NV + v) * N + (PAD ? (ln.vm & 16 ? ln.t : 0) : ln.t));
     } else {
       const int step_d = d == 0 ? 1 : C0;
       const int span = d == 0 ? C0 : C1;
@@ -1027,21 +1053,43 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   double Bx[2][NV], Fyp[2][NV];
   // both nodes of the lane at once: one 16-byte load per (array, var)
   double Up[2][NV];
-  double* sS = sF + NV * NPE;  // last stage: S at the flux nodes, read back at the output nodes
+  double* sS = sF + NV * 64;  // last stage: S at the flux nodes, read back at the output nodes
+  if constexpr (PAD) {
+    // scalar loads (the node pairs of odd N are not 16-byte aligned); a
+    // padded node gets rho = 1, momentum 0 (finite fluxes, zeroed below)
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    if (last) {
-      double S0, S1;
-      combine_pair<NU, AM, BM>(p, ring, src + v * NPE + ln.n0, ebase + v * NPE + ln.n0, CHUNK, Up[0][v], Up[1][v],
-                               &S0, &S1);
-      *reinterpret_cast<double2*>(sS + v * NPE + ln.n0s) = make_double2(S0, S1);
-    } else {
-      combine_pair<NU, AM>(p, ring, src + v * NPE + ln.n0, ebase + v * NPE + ln.n0, CHUNK, Up[0][v], Up[1][v]);
+    for (int h = 0; h < 2; ++h) {
+      const bool ok = (ln.vm >> h & 1) != 0;
+      double Sh[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double Uv = (KIND == 1 && v == 0) ? 1.0 : 0.0, Sv = 0.0;
+        if (ok) combine_g<false, NU, AM, BM>(p, ebase + v * NPE + ln.g0 + h, last, Uv, Sv);
+        Up[h][v] = Uv;
+        Sh[v] = Sv;
+      }
+      if (last) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sS[v * 64 + ln.n0s + h] = Sh[v];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (last) {
+        double S0, S1;
+        combine_pair<NU, AM, BM>(p, ring, src + v * NPE + ln.n0, ebase + v * NPE + ln.n0, CHUNK, Up[0][v],
+                                 Up[1][v], &S0, &S1);
+        *reinterpret_cast<double2*>(sS + v * NPE + ln.n0s) = make_double2(S0, S1);
+      } else {
+        combine_pair<NU, AM>(p, ring, src + v * NPE + ln.n0, ebase + v * NPE + ln.n0, CHUNK, Up[0][v], Up[1][v]);
+      }
     }
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int n = ln.n0 + h;
+    const bool ok = !PAD || (ln.vm >> h & 1) != 0;
     double U[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) U[v] = Up[h][v];
@@ -1052,7 +1100,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       sx = fabs(p.vel[0]);
       sy = fabs(p.vel[1]);
     } else {
-      if (!(U[0] > 0.0)) {
+      if (!(U[0] > 0.0)) {  // (padded nodes hold rho = 1)
         const int i = n & 7, j = n >> 3;
         const long long gx = cx + p.goff[0], gy = cy + p.goff[1];
         record_error(p.ctl, error_key(step, p.phase, (gx * p.gcells[1] + gy) * (long long)p.gcells[2], j * N + i));
@@ -1071,14 +1119,14 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
     }
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      Bx[h][v] = Fx[v];
-      Fyp[h][v] = Fy[v];
+      Bx[h][v] = ok ? Fx[v] : 0.0;
+      Fyp[h][v] = ok ? Fy[v] : 0.0;
     }
     // face traces, U only (the face lane recomputes flux and speed, cheaper
     // than the partial-warp shared stores of keeping them): x faces at
     // i = 2c + h = 0 / 7, y faces at j = r = 0 / 7
     const int i = 2 * ln.c + h;
-    if (i == 0 || i == N - 1) {
+    if ((i == 0 || i == N - 1) && (!PAD || ln.r < N)) {
       double* t = sT + (i == 0 ? 0 : HW) * L + ln.r;
 #pragma unroll
       for (int v = 0; v < NV; ++v) t[v * L] = U[v];
@@ -1102,7 +1150,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
 #endif
 #pragma unroll
   for (int v = 0; v < NV; ++v)
-    *reinterpret_cast<double2*>(sF + v * NPE + ln.n0s) = make_double2(Fyp[0][v], Fyp[1][v]);
+    *reinterpret_cast<double2*>(sF + v * 64 + ln.n0s) = make_double2(Fyp[0][v], Fyp[1][v]);
   __syncwarp();
 
   // ---------------------------------------------------------- faces
@@ -1173,26 +1221,37 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
     double d0 = 0.0, d1 = 0.0;
     dmma_8x8x4(ln.kx[0], Bx[0][v], d0, d1);  // D_x = K_x F_x
     dmma_8x8x4(ln.kx[1], Bx[1][v], d0, d1);
-    const double* Fy = sF + v * NPE;
+    const double* Fy = sF + v * 64;
     dmma_8x8x4(Fy[ln.a0s], ln.ky[0], d0, d1);  // += F_y K_y^T, A = F_y[i=r][j=2c+h]
     dmma_8x8x4(Fy[ln.a1s], ln.ky[1], d0, d1);
-    // lifted face fluxes: x faces on rows r = 0 / 7 (line j), y faces on
-    // columns j = 0 (s = 0 of c = 0) / 7 (s = 1 of c = 3) (line i = r)
+    // lifted face fluxes: x faces on rows r = 0 / N-1 (line j), y faces on
+    // columns j = 0 (s = 0 of c = 0) / N-1 (N = 8: s = 1 of c = 3) (line i = r)
     const double* hx = sH + (ln.xf * NV + v) * L + 2 * ln.c;
     d0 = fma(ln.xco, hx[0], d0);
     d1 = fma(ln.xco, hx[1], d1);
-    d0 = fma(ln.yco0, sH[(2 * NV + v) * L + ln.r], d0);
-    d1 = fma(ln.yco1, sH[(3 * NV + v) * L + ln.r], d1);
-    const double k0 = d0 * dt, k1 = d1 * dt;
-    if (!last) {
-      gout[v * NPE + ln.o0] = k0;
-      gout[v * NPE + ln.o0 + 8] = k1;
+    if constexpr (PAD) {
+      d0 = fma(ln.yco0, sH[(ln.yf0 * NV + v) * L + ln.r], d0);
+      d1 = fma(ln.yco1p, sH[(ln.yf1 * NV + v) * L + ln.r], d1);
     } else {
-      const double S0 = sS[v * NPE + ln.a0s], S1 = sS[v * NPE + ln.a1s];
+      d0 = fma(ln.yco0, sH[(2 * NV + v) * L + ln.r], d0);
+      d1 = fma(ln.yco1, sH[(3 * NV + v) * L + ln.r], d1);
+    }
+    const double k0 = d0 * dt, k1 = d1 * dt;
+    const int o0 = PAD ? ln.og0 : ln.o0, o1 = PAD ? ln.og1 : ln.o0 + 8;
+    const bool w0 = !PAD || (ln.vm & 4) != 0, w1 = !PAD || (ln.vm & 8) != 0;
+    if (!last) {
+      if (w0) gout[v * NPE + o0] = k0;
+      if (w1) gout[v * NPE + o1] = k1;
+    } else {
+      const double S0 = sS[v * 64 + ln.a0s], S1 = sS[v * 64 + ln.a1s];
       un[0][v] = fma(p.b_last, k0, S0);
       un[1][v] = fma(p.b_last, k1, S1);
-      gout[v * NPE + ln.o0] = un[0][v];
-      gout[v * NPE + ln.o0 + 8] = un[1][v];
+      if (w0) gout[v * NPE + o0] = un[0][v];
+      if (w1) gout[v * NPE + o1] = un[1][v];
+      // a padded output node: rho = 1, momentum 0 (finite; its wavespeed a
+      // is below every real node's, so the alpha max is unchanged)
+      if (!w0) un[0][v] = v == 0 ? 1.0 : 0.0;
+      if (!w1) un[1][v] = v == 0 ? 1.0 : 0.0;
     }
   }
   if (last) {
@@ -1240,12 +1299,21 @@ __host__ __device__ constexpr int stage_minb(int dim, int n, int kind, bool exac
 #ifndef NDGX_MINB2
 #define NDGX_MINB2 0x444  // the 2D order-8 Euler flagship, same classes: last (bm != 0) | others | u-only
 #endif
-  // (generic bodies: 2D o4 5 CTAs, 1.03e11 -> 1.05e11 Euler; 2D o6 Euler 3 CTAs, 7.2e10 -> 7.9e10)
+#ifndef NDGX_MINBP
+#define NDGX_MINBP 0x555  // the padded flagship body (2D Euler o5-o7), the same classes
+#endif
+  // (generic bodies: 2D o4 5 CTAs, 1.03e11 -> 1.05e11 Euler; 2D o6 Euler 3 CTAs, 7.2e10 -> 7.9e10;
+  //  2D o5 advection 5 CTAs, 7.6e10 -> 8.1e10.  The padded flagship body at 5 CTAs:
+  //  Euler o5 / o6 / o7 8.1 / 11.9 / 13.9e10 -> 9.0 / 12.2 / 15.5e10, profiles/r02/padded_mma_tune.jsonl)
   return (dim == 3 && n == 4 && kind == 1 && !exact)
              ? (int)((NDGX_MINB3 >> (4 * sig)) & 15)
          : (dim == 2 && n == 8 && kind == 1 && !exact)
              ? (sig == 0 ? (NDGX_MINB2 & 15)
                          : ((kSigs[sig].bm != 0) ? (NDGX_MINB2 >> 8 & 15) : (NDGX_MINB2 >> 4 & 15)))
+         : (dim == 2 && n >= 5 && n < 8 && ((NDGX_MMA2_ORDERS >> n) & 1) != 0 && kind == 1 && !exact)
+             ? (sig == 0 ? (NDGX_MINBP & 15)
+                         : ((kSigs[sig].bm != 0) ? (NDGX_MINBP >> 8 & 15) : (NDGX_MINBP >> 4 & 15)))
+         : (dim == 2 && n == 5 && kind == 0 && !exact) ? 5
          : (dim == 2 && n == 4 && !exact) ? 5
          : (dim == 2 && n == 6 && kind == 1 && !exact) ? 3
                                                         : 4;
@@ -1290,12 +1358,13 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   constexpr bool LASTC = kSigs[SIG].bm != 0;
   constexpr int WSL = G::wslab(USE_MMA || USE_MMA3, LASTC);
   // slab: fluxes (2D MMA: F_y; 3D MMA: F_x|F_y|F_z) | S (last stage) | traces | face fluxes
-  constexpr int OFFT = USE_MMA ? (1 + (LASTC ? 1 : 0)) * NV * NPE
+  constexpr int OFFT = USE_MMA ? (1 + (LASTC ? 1 : 0)) * NV * 64  // (2D: the padded 8 x 8 grid)
                                : (USE_MMA3 ? (3 + (LASTC ? 1 : 0)) * NV * NPE : G::OFF_T);
   constexpr int TRW = USE_MMA3 ? NV + 1 : (USE_MMA ? HW : G::TW);  // trace record width
+  constexpr int LS = USE_MMA ? 8 : L;                              // trace slots per face
   double* sF = smem + G::HEAD + wib * (WSL + depth * SLOT);
-  double* sT = sF + OFFT;                                    // [face][TRW][L]
-  double* sH = sT + G::FACES * TRW * L;                      // [face][NV][L]
+  double* sT = sF + OFFT;                                    // [face][TRW][LS]
+  double* sH = sT + G::FACES * TRW * LS;                     // [face][NV][LS]
   double* ring = sF + WSL;                                   // [depth][1+NU][NV][NPE] | faces
   const long long nwarps = (long long)gridDim.x * G::WARPS;
   double alpha = 0.0;
@@ -1355,7 +1424,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     }
   };
 
-  // MMA lane roles (2D N=8): lane = 4r + c
+  // MMA lane roles (2D, the 8 x 8 grid): lane = 4r + c
   const int r = lane >> 2, c = lane & 3;
   double hc3[KIND == 0 ? 1 : 4] = {};  // line body: the z-hi face flux carried along a z-run
   const double rdy3 = DIM == 3 ? p.lift[1] / p.lift[0] : 1.0, rdz3 = DIM == 3 ? p.lift[2] / p.lift[0] : 1.0;
@@ -1368,11 +1437,12 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   if constexpr (USE_MMA) {
     ln8.r = r;
     ln8.c = c;
-    ln8.n0 = 2 * c + N * r;
+    ln8.n0 = 2 * c + 8 * r;
     ln8.f = lane >> 3;
     ln8.t = lane & 7;
-    // the neighbour's facing node: x-lo (7, t), x-hi (0, t), y-lo (t, 7), y-hi (t, 0)
-    ln8.nb_node = ln8.f == 0 ? 7 + 8 * ln8.t : (ln8.f == 1 ? 8 * ln8.t : (ln8.f == 2 ? ln8.t + 56 : ln8.t));
+    const int tn = ln8.t < N ? ln8.t : 0;  // (a padded face lane reads node 0's address)
+    // the neighbour's facing node: x-lo (N-1, t), x-hi (0, t), y-lo (t, N-1), y-hi (t, 0)
+    ln8.nb_node = ln8.f == 0 ? N - 1 + N * tn : (ln8.f == 1 ? N * tn : (ln8.f == 2 ? tn + N * (N - 1) : tn));
     ln8.o0 = r + 16 * c;
     ln8.n0s = swz8(ln8.n0);
     ln8.a0s = swz8(ln8.o0);
@@ -1382,8 +1452,20 @@ stage_kernel(const __grid_constant__ StageArgs p) {
     ln8.yco0 = c == 0 ? p.lift[1] : 0.0;
     ln8.yco1 = c == 3 ? -p.lift[1] : 0.0;
     for (int h = 0; h < 2; ++h) {
-      ln8.kx[h] = p.K[0][r * N + 2 * c + h];
-      ln8.ky[h] = p.K[1][r * N + 2 * c + h];
+      const bool in = r < N && 2 * c + h < N;
+      ln8.kx[h] = in ? p.K[0][r * N + 2 * c + h] : 0.0;
+      ln8.ky[h] = in ? p.K[1][r * N + 2 * c + h] : 0.0;
+    }
+    if constexpr (N < 8) {
+      ln8.g0 = 2 * c + N * r;
+      ln8.og0 = r + N * 2 * c;
+      ln8.og1 = ln8.og0 + N;
+      ln8.vm = (r < N && 2 * c < N ? 5 : 0) | (r < N && 2 * c + 1 < N ? 10 : 0) | (ln8.t < N ? 16 : 0);
+      // y faces: output (r, j = 2c + s) takes the lo face at j = 0, the hi face at j = N - 1
+      ln8.yf0 = 2 * c == N - 1 ? 3 : 2;
+      ln8.yf1 = 2 * c + 1 == N - 1 ? 3 : 2;
+      ln8.yco0 = 2 * c == 0 ? p.lift[1] : (2 * c == N - 1 ? -p.lift[1] : 0.0);
+      ln8.yco1p = 2 * c + 1 == N - 1 ? -p.lift[1] : 0.0;
     }
   }
 
@@ -1448,7 +1530,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
           // region 3: the rows of the range are interior, only x in [X0, X1) is
           // taken, and the x-lo neighbour is in the slab for x > X0
           if (!XF || (x >= X0 && x < X1))
-            element_2d8_fast<KIND, NU, AM, BM, SIG>(p, ln8, lane, rb + k, x, y, ring, nullptr, false, sF, sT, sH,
+            element_2d8_fast<N, KIND, NU, AM, BM, SIG>(p, ln8, lane, rb + k, x, y, ring, nullptr, false, sF, sT, sH,
                                                     dt, last, step, alpha, k > 0 && x > X0);
           if (++x == C0) {
             x = 0;
@@ -1843,7 +1925,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
 
   // generic body with several elements per warp: chunks of EPW consecutive
   // range elements, chunk c -> warp c mod nw
-  if constexpr (G::GL < 32) {
+  if constexpr (G::GL < 32 && !USE_MMA) {
     const int grp = lane / G::GL;
     const long long cnt = ((long long)nelem - e_lo + e_stride - 1) / e_stride;  // elements of this range
     for (long long c = (long long)blockIdx.x * G::WARPS + wib; c * G::EPW < cnt; c += nw) {
@@ -1895,7 +1977,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       continue;
     }
     if constexpr (USE_MMA) {
-      element_2d8_fast<KIND, NU, AM, BM, SIG>(p, ln8, lane, e, cx, cy, src, fsrc, depth > 0, sF, sT, sH, dt, last, step,
+      element_2d8_fast<N, KIND, NU, AM, BM, SIG>(p, ln8, lane, e, cx, cy, src, fsrc, depth > 0, sF, sT, sH, dt, last, step,
                                          alpha);
       if (depth > 0 && ++slot == depth) {
         slot = 0;

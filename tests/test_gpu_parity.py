@@ -347,8 +347,10 @@ def test_full_size_c4_fast_equals_exact_and_conserves():
     assert abs(tot[0] - t0[0]) <= 1e-12 * abs(t0[0])
 
 
-@pytest.mark.parametrize("dim,cells,order", [(3, (4, 3, 5), 4), (2, (6, 5), 8), (2, (7, 5), 4), (3, (3, 4, 2), 2)],
-                         ids=["3D-o4-lines", "2D-o8-flagship", "2D-o4-groups", "3D-o2-groups"])
+@pytest.mark.parametrize("dim,cells,order", [(3, (4, 3, 5), 4), (2, (6, 5), 8), (2, (7, 5), 4), (3, (3, 4, 2), 2),
+                                             (2, (5, 6), 7), (2, (6, 4), 6)],
+                         ids=["3D-o4-lines", "2D-o8-flagship", "2D-o4-groups", "3D-o2-groups", "2D-o7-padded",
+                              "2D-o6-padded"])
 @pytest.mark.parametrize("arith", [ndgx.ARITH_EXACT, ndgx.ARITH_FAST], ids=["exact", "fast"])
 def test_operator_physics_error_names_the_cell_in_every_body(port, dim, cells, order, arith):
     """A non-positive density at one node: serial_rhs's PhysicsError
@@ -372,6 +374,7 @@ def test_operator_physics_error_names_the_cell_in_every_body(port, dim, cells, o
 @pytest.mark.parametrize("dim,cells,order,kind", [
     (2, (1, 3), 8, EULER), (2, (2, 1), 8, EULER), (2, (1, 1), 8, ADVECTION), (2, (3, 1), 4, EULER),
     (3, (1, 1, 5), 4, EULER), (3, (2, 1, 1), 4, EULER), (3, (1, 2, 1), 4, ADVECTION), (1, (1,), 5, ADVECTION),
+    (2, (1, 3), 7, EULER), (2, (2, 1), 6, ADVECTION), (2, (1, 1), 5, EULER),
 ], ids=lambda x: str(x).replace(" ", ""))
 def test_degenerate_meshes_match_port(port, dim, cells, order, kind):
     """One-cell axes: the element is its own periodic neighbour (and runs,

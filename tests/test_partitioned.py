@@ -47,6 +47,9 @@ CASES = [
     ("2D adv o3 RK3 x-split", (2, (9, 7), 3, False, ndgx.RK3), 3, (3, 1, 1)),
     ("1D adv o4 RK4", (1, (64,), 4, False, ndgx.RK4), 4, (4, 1, 1)),
     ("2D adv o8 RK4 2x2", (2, (12, 12), 8, False, ndgx.RK4), 4, (2, 2, 1)),
+    ("2D Euler o7 RK4 2x2 (padded body)", (2, (10, 12), 7, True, ndgx.RK4), 4, (2, 2, 1)),
+    ("2D Euler o6 RK3 x-split (padded body)", (2, (12, 5), 6, True, ndgx.RK3), 2, (2, 1, 1)),
+    ("2D adv o5 RK6 y-split (padded body)", (2, (6, 12), 5, False, ndgx.RK6), 2, (1, 2, 1)),
 ]
 
 
@@ -123,7 +126,9 @@ def test_partitioned_euler_t_end_fast_equals_single():
 
 @pytest.mark.parametrize("dim,cells,order,euler,rk", [(2, (12, 10), 8, True, ndgx.RK4),
                                                       (3, (5, 4, 6), 4, True, ndgx.RK6),
-                                                      (2, (7, 9), 5, False, ndgx.RK3)])
+                                                      (2, (7, 9), 5, False, ndgx.RK3),
+                                                      (2, (9, 7), 7, True, ndgx.RK4),
+                                                      (2, (6, 8), 6, True, ndgx.RK6)])
 def test_one_worker_forced_through_the_halo_planes(dim, cells, order, euler, rk):
     """Every axis of a single block routed through its own halo planes (the
     boxes: interior + a shell on every axis) is the single-block run."""
