@@ -20,7 +20,11 @@ CASES = [
     ("3D Euler o4 RK6 fast, 16 z planes (line body, z-runs of 8)", 3, (3, 2, 16), 4, True, ndgx.RK6,
      ndgx.ARITH_FAST, None),
     ("2D Euler o8 exact (line-task volume)", 2, (5, 4), 8, True, ndgx.RK4, ndgx.ARITH_EXACT, None),
-    ("2D Euler o6 fast (whole-line volume, 8 lanes per element)", 2, (7, 5), 6, True, ndgx.RK4, ndgx.ARITH_FAST,
+    ("2D Euler o6 fast (flagship body zero-padded to 8 x 8, x-runs)", 2, (7, 5), 6, True, ndgx.RK4, ndgx.ARITH_FAST,
+     None),
+    ("2D Euler o7 fast (flagship body zero-padded, odd N)", 2, (5, 6), 7, True, ndgx.RK6, ndgx.ARITH_FAST, None),
+    ("2D advection o7 fast (flagship body zero-padded)", 2, (4, 5), 7, False, ndgx.RK4, ndgx.ARITH_FAST, None),
+    ("2D Euler o6 exact (whole-line volume, 8 lanes per element)", 2, (7, 5), 6, True, ndgx.RK4, ndgx.ARITH_EXACT,
      None),
     ("2D advection o7 exact (whole-line volume)", 2, (4, 3), 7, False, ndgx.RK3, ndgx.ARITH_EXACT, None),
 ]
