@@ -58,6 +58,9 @@ namespace ndgx {
 #ifndef NDGX_GPF
 #define NDGX_GPF 1  // generic body: all of a lane's node loads issued before any combination
 #endif
+#ifndef NDGX_DT2
+#define NDGX_DT2 1  // flagship Euler, stages without b-terms: transposed volume product (outputs at own node pair)
+#endif
 #ifndef NDGX_YTR2
 #define NDGX_YTR2 1  // flagship: y-face traces as one 16-byte store per variable
 #endif
@@ -987,6 +990,12 @@ struct Lane8 {
   int vm;                // valid bits: 1, 2 flux nodes h = 0, 1; 4, 8 output nodes s = 0, 1; 16 face node t
   int yf0, yf1;          // y face (2 lo / 3 hi) lifted into output s = 0 / 1
   double yco1p;          // its coefficient for s = 1 (yco0 for s = 0)
+  // transposed output (NDGX_DT2): the lane's outputs are its own flux nodes
+  // (i = 2c + s, j = r); the y face of row r is shared, the x face is per s
+  double gco;            // y-face lift coefficient of row r (0 inside)
+  int gf;                // its face (2 lo / 3 hi)
+  double fco0, fco1;     // x-face lift coefficients of outputs s = 0 / 1
+  int ff0, ff1;          // their faces (0 lo / 1 hi)
 };
 
 // Slab slot of node n = i + 8 j for the flagship's F_y and S arrays: the
@@ -1216,6 +1225,52 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   // ---------------------------------------------------------- volume + epilogue
   double* gout = p.out + ebase;
   double un[2][NV];
+  // Euler stages without b-terms: D^T = F_x^T K_x^T + K_y F_y^T, the same
+  // fragments with the operands swapped, so the accumulator holds D at the
+  // lane's own flux nodes (i = 2c + s, j = r), n0 and n0 + 1: one 16-byte
+  // store per variable instead of two 8-byte ones.  Measured (profiles/r02/
+  // dt2_ab.jsonl): C3 2.237 -> 2.184 ms/step, C5 18.45 -> 17.90; the last
+  // stages (more spills: C5 6.35 -> 6.89 ms) and advection (C2 1-term stages
+  // 0.069 -> 0.079 ms) lose, so they keep D.
+  constexpr bool DT = NDGX_DT2 != 0 && KIND == 1 && BM == 0;
+  const int on0 = DT ? ln.n0 : ln.o0;  // output node s: on0 + s * ostep (slab index i + 8 j)
+  constexpr int ostep = DT ? 1 : 8;
+  if constexpr (DT) {
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double d0 = 0.0, d1 = 0.0;
+    dmma_8x8x4(Bx[0][v], ln.kx[0], d0, d1);  // A = F_x^T (own fluxes), B = K_x^T
+    dmma_8x8x4(Bx[1][v], ln.kx[1], d0, d1);
+    const double* Fy = sF + v * 64;
+    dmma_8x8x4(ln.ky[0], Fy[ln.a0s], d0, d1);  // A = K_y, B = F_y^T (F_y[i=r][j=2c+h])
+    dmma_8x8x4(ln.ky[1], Fy[ln.a1s], d0, d1);
+    // lifted face fluxes: y faces on rows r = 0 / N-1 (line i), x faces on
+    // columns i = 0 / N-1 (line j = r)
+    const double* hy = sH + (ln.gf * NV + v) * L + 2 * ln.c;
+    d0 = fma(ln.gco, hy[0], d0);
+    d1 = fma(ln.gco, hy[1], d1);
+    d0 = fma(ln.fco0, sH[((PAD ? ln.ff0 : 0) * NV + v) * L + ln.r], d0);
+    d1 = fma(ln.fco1, sH[((PAD ? ln.ff1 : 1) * NV + v) * L + ln.r], d1);
+    double o0 = d0 * dt, o1 = d1 * dt;
+    if (last) {
+      const double2 S = *reinterpret_cast<const double2*>(sS + v * 64 + ln.n0s);
+      o0 = fma(p.b_last, o0, S.x);
+      o1 = fma(p.b_last, o1, S.y);
+    }
+    if constexpr (PAD) {
+      if (ln.vm & 1) gout[v * NPE + ln.g0] = o0;
+      if (ln.vm & 2) gout[v * NPE + ln.g0 + 1] = o1;
+      // a padded output node: rho = 1, momentum 0 (finite; its wavespeed a
+      // is below every real node's, so the alpha max is unchanged)
+      un[0][v] = (ln.vm & 1) ? o0 : (v == 0 ? 1.0 : 0.0);
+      un[1][v] = (ln.vm & 2) ? o1 : (v == 0 ? 1.0 : 0.0);
+    } else {
+      *reinterpret_cast<double2*>(gout + v * NPE + ln.n0) = make_double2(o0, o1);
+      un[0][v] = o0;
+      un[1][v] = o1;
+    }
+  }
+  } else {
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     double d0 = 0.0, d1 = 0.0;
@@ -1254,6 +1309,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       if (!w1) un[1][v] = v == 0 ? 1.0 : 0.0;
     }
   }
+  }
   if (last) {
 #pragma unroll
     for (int s2 = 0; s2 < 2; ++s2) {
@@ -1263,7 +1319,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       if (!isfinite(sum)) record_error(p.ctl, error_key(step, kPhaseInstability, p.block_id, 0));
       if (KIND == 1 && p.scan_alpha) {
         if (!(un[s2][0] > 0.0)) {
-          const int n = ln.o0 + 8 * s2;
+          const int n = on0 + ostep * s2;
           const long long gx = cx + p.goff[0], gy = cy + p.goff[1];
           record_error(p.ctl, error_key(step + 1, kPhaseScan, (gx * p.gcells[1] + gy) * (long long)p.gcells[2],
                                         (n & 7) * N + (n >> 3)));
@@ -1467,6 +1523,12 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       ln8.yco0 = 2 * c == 0 ? p.lift[1] : (2 * c == N - 1 ? -p.lift[1] : 0.0);
       ln8.yco1p = 2 * c + 1 == N - 1 ? -p.lift[1] : 0.0;
     }
+    ln8.gco = r == 0 ? p.lift[1] : (r == N - 1 ? -p.lift[1] : 0.0);
+    ln8.gf = r == N - 1 ? 3 : 2;
+    ln8.fco0 = 2 * c == 0 ? p.lift[0] : (2 * c == N - 1 ? -p.lift[0] : 0.0);
+    ln8.fco1 = 2 * c + 1 == N - 1 ? -p.lift[0] : 0.0;
+    ln8.ff0 = 2 * c == N - 1 ? 1 : 0;
+    ln8.ff1 = 1;
   }
 
   // element e = cx + C0 (cy + C1 cz), advanced by the total warp count times
