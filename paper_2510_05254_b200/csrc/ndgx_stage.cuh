@@ -61,6 +61,9 @@ namespace ndgx {
 #ifndef NDGX_DT2
 #define NDGX_DT2 1  // flagship Euler, stages without b-terms: transposed volume product (outputs at own node pair)
 #endif
+#ifndef NDGX_DT2_LAST
+#define NDGX_DT2_LAST 0  // (tuning) the transposed product in the last stages too
+#endif
 #ifndef NDGX_YTR2
 #define NDGX_YTR2 1  // flagship: y-face traces as one 16-byte store per variable
 #endif
@@ -1232,7 +1235,7 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   // dt2_ab.jsonl): C3 2.237 -> 2.184 ms/step, C5 18.45 -> 17.90; the last
   // stages (more spills: C5 6.35 -> 6.89 ms) and advection (C2 1-term stages
   // 0.069 -> 0.079 ms) lose, so they keep D.
-  constexpr bool DT = NDGX_DT2 != 0 && KIND == 1 && BM == 0;
+  constexpr bool DT = NDGX_DT2 != 0 && KIND == 1 && (BM == 0 || NDGX_DT2_LAST != 0);
   const int on0 = DT ? ln.n0 : ln.o0;  // output node s: on0 + s * ostep (slab index i + 8 j)
   constexpr int ostep = DT ? 1 : 8;
   if constexpr (DT) {
