@@ -15,7 +15,8 @@ KERNELS = [("ndgx_inst_d2_o8_e0.o", 2, 8, 1, 0, (0, 1, 3), "C3 flagship: 2D Eule
            ("ndgx_inst_d2_o8_e0.o", 2, 8, 0, 0, (0, 1, 3), "C2: 2D advection o8 RK4 (DMMA body)"),
            ("ndgx_inst_d3_o4_e0.o", 3, 4, 1, 0, (0, 1, 4, 5, 6, 7, 8), "C4: 3D Euler o4 RK6 (DMMA body)"),
            ("ndgx_inst_d2_o8_e1.o", 2, 8, 1, 1, (0, 1, 3), "C3 exact mode (generic body)"),
-           ("ndgx_inst_d2_o4_e0.o", 2, 4, 1, 0, (0, 1, 3), "2D Euler o4 (generic body, 8 lanes per element)")]
+           ("ndgx_inst_d2_o4_e0.o", 2, 4, 1, 0, (0, 1, 3), "2D Euler o4 (generic body, 8 lanes per element)"),
+           ("ndgx_inst_d2_o7_e0.o", 2, 7, 1, 0, (0, 1, 3), "2D Euler o7 (flagship body zero-padded to 8 x 8)")]
 KEYS = ["DMMA", "DFMA", "DMUL", "DADD", "MUFU", "LDG", "STG", "LDS", "STS", "LDL", "STL", "UBLKCP", "LDGSTS",
         "SYNCS", "SHFL", "BAR", "WARPSYNC", "BRA", "BSSY", "IMAD", "ISETP", "LOP3"]
 
