@@ -1838,7 +1838,10 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       double res[4][NV];
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const int k = 4 * half + kk;
+        // the halves interleave (k = 2 kk + half): the in-place stores below
+        // then hit 16 distinct bank pairs per half-warp (k = 4 half + kk put
+        // both halves on the same pairs: 4 wavefronts per store, 2 excessive)
+        const int k = 2 * kk + half;
         const double* Kr = sK + (d * N + k) * G::KROW;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
@@ -1856,7 +1859,7 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       __syncwarp();  // every line's flux reads precede the in-place stores
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const int k = 4 * half + kk;
+        const int k = 2 * kk + half;
 #pragma unroll
         for (int v = 0; v < NV; ++v) gF[(d * NV + v) * NPE + (d == 0 ? sx8(k + 8 * t) : t + 8 * k)] = res[kk][v];
       }
