@@ -1008,11 +1008,58 @@ struct Lane8 {
 // per half-warp instead of two (a 4-way conflict unswizzled).
 __host__ __device__ constexpr int swz8(int n) { return n ^ (((n >> 4) & 3) << 2); }
 
-template <int N, int KIND, int NU, int AM, int BM, int SIG>
+// One element's raw inputs for the flagship body, loaded one element ahead
+// (NDGX_PF2: the advection stages, whose warps otherwise wait one full
+// memory latency per element): the lane's node pair of every input array
+// and its face node's neighbour values.
+template <int NV, int NU>
+struct Pre8 {
+  double2 node[NV][1 + NU];
+  double face[1 + NU][NV];
+};
+
+// The loads of element_2d8_fast (order 8, no ring, no slab reuse), issued
+// into `q` without waiting for them.
+template <int KIND, int NU>
+__device__ __forceinline__ void preload_2d8(const StageArgs& p, const Lane8& ln, int e, int cx, int cy,
+                                            Pre8<KIND == 0 ? 1 : 3, NU>& q) {
+  constexpr int NV = KIND == 0 ? 1 : 3, NPE = 64, N = 8, CHUNK = NV * NPE;
+  const int C0 = p.cells[0], C1 = p.cells[1];
+  const int f = ln.f, d = f >> 1, side = f & 1;
+  const bool bnd = d == 0 ? (side ? cx == C0 - 1 : cx == 0) : (side ? cy == C1 - 1 : cy == 0);
+  const double* ext = p.ext[d][side];
+  if (bnd && ext != nullptr) {
+    const size_t xs = d == 0 ? (size_t)cy : (size_t)cx;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) q.face[0][v] = __ldg(ext + (xs * NV + v) * N + ln.t);
+  } else {
+    const int step_d = d == 0 ? 1 : C0;
+    const int span = d == 0 ? C0 : C1;
+    const int en = side ? (bnd ? e - (span - 1) * step_d : e + step_d) : (bnd ? e + (span - 1) * step_d : e - step_d);
+    const size_t g = (size_t)en * CHUNK + ln.nb_node;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      q.face[0][v] = __ldg(p.u + g + v * NPE);
+#pragma unroll
+      for (int a = 0; a < NU; ++a) q.face[1 + a][v] = __ldg(p.ku[a] + g + v * NPE);
+    }
+  }
+  const size_t ebase = (size_t)e * CHUNK;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const size_t g = ebase + v * NPE + ln.n0;
+    q.node[v][0] = __ldg(reinterpret_cast<const double2*>(p.u + g));
+#pragma unroll
+    for (int t = 0; t < NU; ++t) q.node[v][1 + t] = __ldg(reinterpret_cast<const double2*>(p.ku[t] + g));
+  }
+}
+
+template <int N, int KIND, int NU, int AM, int BM, int SIG, bool PRE = false>
 __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8& ln, int lane, int e, int cx,
                                                  int cy, const double* src, const double* fsrc, bool ring_,
                                                  double* sF, double* sT, double* sH, double dt, bool last,
-                                                 long long step, double& alpha, bool reuse_lo = false) {
+                                                 long long step, double& alpha, bool reuse_lo = false,
+                                                 const Pre8<KIND == 0 ? 1 : 3, NU>* pre = nullptr) {
   // N < 8: the same body on the zero-padded 8 x 8 grid (slab index i + 8 j)
   constexpr bool PAD = N < 8;
   constexpr int NPE = N * N, L = 8;
@@ -1042,7 +1089,12 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
   }
   if (reuse_lo) __syncwarp();  // read before the node phase's trace stores
   double Nraw[1 + NU][NV];
-  if (!ring && !from_prev) {
+  if constexpr (PRE) {
+#pragma unroll
+    for (int a = 0; a < 1 + NU; ++a)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Nraw[a][v] = pre->face[a][v];
+  } else if (!ring && !from_prev) {
     if (from_ext) {
       const size_t xs = d == 0 ? (size_t)cy : (size_t)cx;
 #pragma unroll
@@ -1083,6 +1135,30 @@ __device__ __forceinline__ void element_2d8_fast(const StageArgs& p, const Lane8
       if (last) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) sS[v * 64 + ln.n0s + h] = Sh[v];
+      }
+    }
+  } else if constexpr (PRE) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const double2* k = pre->node[v];
+      double u0 = k[0].x, u1 = k[0].y;
+#pragma unroll
+      for (int t = 0; t < NU; ++t)
+        if ((AM >> t & 1) != 0) {
+          u0 = fma(p.ca[t], k[1 + t].x, u0);
+          u1 = fma(p.ca[t], k[1 + t].y, u1);
+        }
+      Up[0][v] = u0;
+      Up[1][v] = u1;
+      if (last) {  // S = u + sum b_j K_j (combine_pair's expressions)
+        double a = k[0].x, b = k[0].y;
+#pragma unroll
+        for (int t = 0; t < NU; ++t)
+          if ((BM >> t & 1) != 0) {
+            a = fma(p.cb[t], k[1 + t].x, a);
+            b = fma(p.cb[t], k[1 + t].y, b);
+          }
+        *reinterpret_cast<double2*>(sS + v * NPE + ln.n0s) = make_double2(a, b);
       }
     }
   } else {
@@ -2004,6 +2080,47 @@ stage_kernel(const __grid_constant__ StageArgs p) {
       generic_element(ee, x, y, z, nullptr, nullptr, have && !skipped(x, y, z));
     }
     e = nelem;  // done: skip the element loop below
+  }
+#ifndef NDGX_PF2
+#define NDGX_PF2 1
+#endif
+  // advection flagship: each element's loads issued one element ahead (two
+  // register buffers, alternating), so a warp's memory latency overlaps the
+  // previous element's work.  Measured (profiles/r02/c2_prefetch_ab.jsonl):
+  // C2 0.277 -> 0.241 ms/step, advection o8 at 1e8 DOF 1.54e11 -> 1.80e11.
+  // The Euler stages are L1/LSU-bound and lose (C3 2.168 -> 2.193 ms at 3
+  // CTAs/SM, spills at 4: negative/c3_c5_euler_prefetch.jsonl).
+#ifndef NDGX_PF2_EULER
+#define NDGX_PF2_EULER 0
+#endif
+  if constexpr (USE_MMA && N == 8 && NDGX_PF2 != 0 && NU <= 3 &&  // (5+ arrays spill)
+                (KIND == 0 || (NDGX_PF2_EULER != 0 && ((NDGX_XRUN_SIGS >> SIG) & 1) == 0))) {
+    if (depth == 0 && p.region == 0) {
+      Pre8<NV, NU> qa, qb;
+      if (e < nelem) preload_2d8<KIND, NU>(p, ln8, e, cx, cy, qa);
+      while (e < nelem) {
+        int x2 = cx, y2 = cy, z2 = cz;
+        step_coords(x2, y2, z2);
+        const int e2 = e + es;
+        if (e2 < nelem) preload_2d8<KIND, NU>(p, ln8, e2, x2, y2, qb);
+        element_2d8_fast<N, KIND, NU, AM, BM, SIG, true>(p, ln8, lane, e, cx, cy, nullptr, nullptr, false, sF, sT, sH,
+                                                         dt, last, step, alpha, false, &qa);
+        e = e2;
+        cx = x2;
+        cy = y2;
+        cz = z2;
+        if (e >= nelem) break;
+        step_coords(x2, y2, z2);
+        const int e3 = e + es;
+        if (e3 < nelem) preload_2d8<KIND, NU>(p, ln8, e3, x2, y2, qa);
+        element_2d8_fast<N, KIND, NU, AM, BM, SIG, true>(p, ln8, lane, e, cx, cy, nullptr, nullptr, false, sF, sT, sH,
+                                                         dt, last, step, alpha, false, &qb);
+        e = e3;
+        cx = x2;
+        cy = y2;
+        cz = z2;
+      }
+    }
   }
   for (; e < nelem; e += es) {
     const double* src = ring + slot * SLOT;  // this element's u and K_j (when depth > 0)
