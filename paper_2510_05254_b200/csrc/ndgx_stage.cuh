@@ -1651,8 +1651,8 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   // (measured per stage: a win for the Euler last stage, 0.96 -> 0.83 ms on
   // C3, whose x-lo reuse saves two arrays' face loads; a loss elsewhere)
 #ifndef NDGX_XRUN_SIGS
-#define NDGX_XRUN_SIGS 0x109  // the u-only stage (C3 0.50 -> 0.48 ms) and the last stages (bm != 0)
-#endif
+#define NDGX_XRUN_SIGS 0x108  // the last stages (bm != 0); the u-only stage had them (0.50 -> 0.48 ms)
+#endif                        // until one-ahead loads beat them (NDGX_PF2_SIGS below)
   if constexpr (USE_MMA && NDGX_XRUN > 1 && KIND == 1 && ((NDGX_XRUN_SIGS >> SIG) & 1) != 0) {
     // (unfiltered contiguous launches, or x-filtered ones in the XF
     // instantiation: a region test inside the runs perturbs this
@@ -2088,13 +2088,20 @@ stage_kernel(const __grid_constant__ StageArgs p) {
   // register buffers, alternating), so a warp's memory latency overlaps the
   // previous element's work.  Measured (profiles/r02/c2_prefetch_ab.jsonl):
   // C2 0.277 -> 0.241 ms/step, advection o8 at 1e8 DOF 1.54e11 -> 1.80e11.
-  // The Euler stages are L1/LSU-bound and lose (C3 2.168 -> 2.193 ms at 3
-  // CTAs/SM, spills at 4: negative/c3_c5_euler_prefetch.jsonl).
+  // The Euler u-only stage waits on its node loads (35% of its samples at
+  // the first use of U) and takes it too, in place of its x-runs: C3 2.173 ->
+  // 2.145, C5 17.74 -> 17.58 ms/step (medians of 5, c3_stage0_prefetch_ab.jsonl).
+  // The other Euler stages are L1/LSU-bound and lose (C3 2.168 -> 2.193 ms
+  // at 3 CTAs/SM, spills at 4: negative/c3_c5_euler_prefetch.jsonl).
 #ifndef NDGX_PF2_EULER
-#define NDGX_PF2_EULER 0
+#define NDGX_PF2_EULER 1
+#endif
+#ifndef NDGX_PF2_SIGS
+#define NDGX_PF2_SIGS 0x1  // the Euler signatures it applies to: the u-only stage
 #endif
   if constexpr (USE_MMA && N == 8 && NDGX_PF2 != 0 && NU <= 3 &&  // (5+ arrays spill)
-                (KIND == 0 || (NDGX_PF2_EULER != 0 && ((NDGX_XRUN_SIGS >> SIG) & 1) == 0))) {
+                (KIND == 0 || (NDGX_PF2_EULER != 0 && ((NDGX_PF2_SIGS >> SIG) & 1) != 0 &&
+                               ((NDGX_XRUN_SIGS >> SIG) & 1) == 0))) {
     if (depth == 0 && p.region == 0) {
       Pre8<NV, NU> qa, qb;
       if (e < nelem) preload_2d8<KIND, NU>(p, ln8, e, cx, cy, qa);
