@@ -128,10 +128,13 @@ def test_partitioned_euler_t_end_fast_equals_single():
                                                       (3, (5, 4, 6), 4, True, ndgx.RK6),
                                                       (2, (7, 9), 5, False, ndgx.RK3),
                                                       (2, (9, 7), 7, True, ndgx.RK4),
-                                                      (2, (6, 8), 6, True, ndgx.RK6)])
+                                                      (2, (6, 8), 6, True, ndgx.RK6),
+                                                      (2, (1067, 3), 8, True, ndgx.RK4),
+                                                      (2, (1101, 2), 8, True, ndgx.RK6)])
 def test_one_worker_forced_through_the_halo_planes(dim, cells, order, euler, rk):
     """Every axis of a single block routed through its own halo planes (the
-    boxes: interior + a shell on every axis) is the single-block run."""
+    boxes: interior + a shell on every axis) is the single-block run, also
+    on 1000+-wide meshes (x-runs straddling rows, RK6 last stage)."""
     cfg = _cfg(dim, cells, order, euler, rk)
     u0 = _u0(cfg)
     plan = ndgx.StepPlan(6, False)
