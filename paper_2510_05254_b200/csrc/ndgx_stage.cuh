@@ -1437,14 +1437,21 @@ __host__ __device__ constexpr int stage_minb(int dim, int n, int kind, bool exac
 #ifndef NDGX_MINBP
 #define NDGX_MINBP 0x555  // the padded flagship body (2D Euler o5-o7), the same classes
 #endif
+#ifndef NDGX_MINBA
+#define NDGX_MINBA 0x445  // the 2D order-8 advection flagship (C2), the same classes
+#endif
   // (generic bodies: 2D o4 5 CTAs, 1.03e11 -> 1.05e11 Euler; 2D o6 Euler 3 CTAs, 7.2e10 -> 7.9e10;
-  //  2D o5 advection 5 CTAs, 7.6e10 -> 8.1e10.  The padded flagship body at 5 CTAs:
+  //  2D o5 advection 5 CTAs, 7.6e10 -> 8.1e10.  The advection flagship's u-only
+  //  stage at 5 CTAs: C2 stage 0 0.0505 -> 0.0463 ms (profiles/r02/c2_caps_after_prefetch.jsonl).  The padded flagship body at 5 CTAs:
   //  Euler o5 / o6 / o7 8.1 / 11.9 / 13.9e10 -> 9.0 / 12.2 / 15.5e10, profiles/r02/padded_mma_tune.jsonl)
   return (dim == 3 && n == 4 && kind == 1 && !exact)
              ? (int)((NDGX_MINB3 >> (4 * sig)) & 15)
          : (dim == 2 && n == 8 && kind == 1 && !exact)
              ? (sig == 0 ? (NDGX_MINB2 & 15)
                          : ((kSigs[sig].bm != 0) ? (NDGX_MINB2 >> 8 & 15) : (NDGX_MINB2 >> 4 & 15)))
+         : (dim == 2 && n == 8 && kind == 0 && !exact)
+             ? (sig == 0 ? (NDGX_MINBA & 15)
+                         : ((kSigs[sig].bm != 0) ? (NDGX_MINBA >> 8 & 15) : (NDGX_MINBA >> 4 & 15)))
          : (dim == 2 && n >= 5 && n < 8 && ((NDGX_MMA2_ORDERS >> n) & 1) != 0 && kind == 1 && !exact)
              ? (sig == 0 ? (NDGX_MINBP & 15)
                          : ((kSigs[sig].bm != 0) ? (NDGX_MINBP >> 8 & 15) : (NDGX_MINBP >> 4 & 15)))
