@@ -14,9 +14,9 @@
 //
 // Arithmetic: every entry takes `arith` last.  The default NDGX_ARITH_EXACT
 // is bit-identical to the reference (the reference's unfused operation
-// order: 1.02e11 DOF*stage/s on C3).  NDGX_ARITH_FAST (FMA contraction, FP64
+// order: 1.03e11 DOF*stage/s on C3).  NDGX_ARITH_FAST (FMA contraction, FP64
 // tensor cores; <= 1e-12 relative L2 vs the reference) is the headline
-// throughput, 2.10e11 -- pass it explicitly.
+// throughput, 2.12e11 -- pass it explicitly.
 //
 // with the same argument meaning, return types and exceptions
 // (include/ndg/errors.hpp:13-56).  The operator coefficients are built from
